@@ -1,0 +1,362 @@
+"""Benchmark: the reference's full timestep (config 5) on B200.
+
+Workload (BASELINE.json config 5, restated in SURVEY.md §8(d)): 128^3-cell
+periodic unigrid = 4096 subgrids of 8^3, rotating polytrope (floor 0.05),
+gamma 1.4, theta 0.34, eps 0.5, expansion order 1.  One bench step = one
+reference timestep (driver.py:163-174): mass = rho*dx^3, 6 x (ghost fill +
+cluster aggregation + P2P + M2L), max wave speed + dt, 3 x (ghost fill +
+reconstruct + flux + update).  z-slabs over N GPUs (NCCL halo + MAX
+all-reduce), strong scaling.
+
+value = subgrids advanced one full timestep per second, whole job
+        (4096 * steps / max-over-ranks device time), inputs resident in HBM.
+e2e   = same unit through the public host API: every step uploads the state
+        from pinned host memory, runs the step and reads the new state and
+        gravity back (H2D/D2H inside the timed region).
+per_kernel: subgrids/s and mean launch time of every kernel inside the timed
+        steps (CUDA events on the launching stream).
+roofline: M2L (the dominant kernel), algorithmic FLOPs (SURVEY.md §8(d):
+        26,800,128 per subgrid at order 1) / mean launch time, against the
+        FP64 peak measured in this run by a DFMA microbenchmark (no FP64
+        entry exists in MEASURED_PEAKS.json).
+cpu_baseline: the C restatement of the reference kernels (oracle/, built
+        -march=native on this host) on all host threads, timed on a bounded
+        sample of the same workload and extrapolated to a full step.
+
+`--impl reference` times that CPU implementation alone (rank 0) with the same
+metric/config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "FP64 subgrids/s per kernel (M2L, P2P, hydro) at 1/2/4/8 B200; % FP64/HBM roofline"
+UNIT = "subgrids/s"
+M2L_FLOP = {1: 26_800_128, 0: 8_338_944}      # SURVEY.md §8(d), per subgrid
+P2P_FLOP = 423_936
+HYDRO_ITER_FLOP = 1_174_000 + 1_275_264 + 17_920   # reconstruct + flux + update
+LEVEL = 4
+
+
+def config_dict(world: int) -> dict:
+    return {"workload": "config5: full timestep, 128^3 unigrid (4096 subgrids of 8^3), 6x(P2P+M2L) + 3x hydro",
+            "level": LEVEL, "subgrids": 8 ** LEVEL, "theta": 0.34, "eps": 0.5, "expansion_order": 1,
+            "gamma": 1.4, "floor": 0.05, "omega": 0.1, "parallelism": f"zslab{world}",
+            "l2": "per-step working set > L2 (Q buffer 4.26 GB/step); no explicit flush"}
+
+
+# -- clocks ---------------------------------------------------------------------
+
+REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+class ClockSampler:
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.out = None
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm,power.draw," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is None:
+            return
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        self.out = out
+
+    def summary(self) -> dict:
+        if not self.out:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons, power = [], [], set(), []
+        for line in self.out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 3 + len(REASONS):
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+                power.append(float(f[2]))
+            except ValueError:
+                continue
+            for r, v in zip(REASONS, f[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(r)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+# -- CPU baseline (oracle) --------------------------------------------------------
+
+def cpu_sample(state: dict, level: int, threads: int, m2l_leaves: int) -> dict:
+    """Time the CPU restatement of the reference kernels on a bounded sample
+    of the config-5 workload; return per-kernel rates and the extrapolated
+    full-step rate (subgrids/s)."""
+    from oracle import oracle as O
+    n = 8 << level
+    dx = 1.0 / n
+    allc = O.leaf_coords(level)
+    rng = np.random.default_rng(5)
+    U = np.stack([state[k] for k in O.HYDRO_FIELDS])
+    mass = U[0] * dx ** 3
+    pick = np.ascontiguousarray(allc[rng.choice(len(allc), size=min(m2l_leaves, len(allc)), replace=False)])
+    sample512 = np.ascontiguousarray(allc[rng.choice(len(allc), size=512, replace=False)])
+    t = {}
+    t0 = time.perf_counter()
+    O.m2l_batch(mass, dx, 0.34, 0.5, 1, pick, threads)
+    t["m2l"] = len(pick) / (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    O.p2p_batch(mass, dx, 0.34, 0.5, sample512, threads)
+    t["p2p"] = 512 / (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    O.wavespeed_batch(U, 1.4, 1e-12, sample512, threads)
+    t["max_wavespeed"] = 512 / (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    O.hydro_batch(U, 1e-12, 1.4, 1e-4, sample512, threads)
+    t["hydro"] = 512 / (time.perf_counter() - t0)
+    nl = len(allc)
+    step_s = 6 * (nl / t["m2l"] + nl / t["p2p"]) + nl / t["max_wavespeed"] + 3 * nl / t["hydro"]
+    return {"rates": t, "step_s": step_s, "value": nl / step_s,
+            "sample": f"M2L on {len(pick)} random leaves, P2P/wavespeed/hydro iteration on 512 leaves of "
+                      f"the config-5 state; full 4096-leaf step extrapolated as 6*(M2L+P2P)+ws+3*hydro"}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2210_06439_b200 import scenarios
+    kind = "port-native" if O.use_native() else "port"
+    threads = O.max_threads()
+    state = scenarios.config5_state(LEVEL)
+    m2l_leaves = max(2 * threads, 32)
+    for _ in range(args.warmup):
+        cpu_sample(state, LEVEL, threads, m2l_leaves)
+    vals, steps = [], []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = cpu_sample(state, LEVEL, threads, m2l_leaves)
+        vals.append(r["value"])
+        steps.append(r["step_s"])
+    wall = time.perf_counter() - t0
+    value = statistics.median(vals)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": statistics.median(steps) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (config-5 IC)",
+        "impl": "reference",
+        "config": config_dict(world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "build": kind, "sample": r["sample"], "rates": r["rates"],
+                         "wall_s_timed": wall},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference arm = the oracle's C restatement of the reference numba kernels "
+                "(bit-identical to it, tests/test_oracle_golden.py), all host threads; "
+                "step time extrapolated from a bounded sample",
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -- our arm ------------------------------------------------------------------------
+
+def fp64_peak(torch) -> dict:
+    import ctypes
+
+    from paper_2210_06439_b200 import _lib
+    L = _lib.load()
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    res = {}
+    for mode, name in ((0, "dfma_tflops"), (1, "dadd_tflops")):
+        best = 0.0
+        for rep in range(4):
+            flops = ctypes.c_int64()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            rc = L.sg_fp64_peak(mode, 2000, sink.data_ptr(), ctypes.byref(flops),
+                                torch.cuda.current_stream().cuda_stream)
+            e.record()
+            torch.cuda.synchronize()
+            if rc:
+                raise RuntimeError(L.sg_last_error().decode())
+            if rep:
+                best = max(best, flops.value / (s.elapsed_time(e) * 1e-3) / 1e12)
+        res[name] = best
+    return res
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_06439_b200 import _lib, grid, scenarios
+    from paper_2210_06439_b200.kernels import GravityConfig, HydroConfig
+    from paper_2210_06439_b200.slab import Slab
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    slab = Slab(LEVEL, rank, world)
+    state = scenarios.config5_state(LEVEL)
+    peaks = fp64_peak(torch)
+
+    u = grid.UnigridState(LEVEL, HydroConfig(gamma=1.4), GravityConfig(theta=0.34, eps=0.5, expansion_order=1),
+                          slab=slab, group=group)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    u.load(state)
+    for _ in range(args.warmup):
+        u.step()
+    u.check_errors()
+    u.load(state)
+    barrier()
+    gpu_uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+    u.timers = {}
+    launches0 = _lib.LAUNCHES["count"]
+    with ClockSampler(gpu_uuid) as clk:
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_ev.record()
+        for _ in range(args.steps):
+            u.step()
+        e_ev.record()
+        barrier()
+    launches = _lib.LAUNCHES["count"] - launches0
+    elapsed = s_ev.elapsed_time(e_ev) * 1e-3
+    u.check_errors()
+    per_kernel = {}
+    for name, evs in u.timers.items():
+        ts = [a.elapsed_time(b) * 1e-3 for a, b in evs]
+        per_kernel[name] = {"launches": len(ts), "mean_ms": 1e3 * sum(ts) / len(ts),
+                            "subgrids_per_s": u.nleaves * world * len(ts) / sum(ts)}
+    u.timers = None
+    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = t.item()
+    total_leaves = 8 ** LEVEL
+    value = total_leaves * args.steps / elapsed
+
+    # e2e through the public host API (pinned host buffers, copies timed)
+    host_in = {k: torch.from_numpy(np.ascontiguousarray(state[k][slab.z0:slab.z0 + slab.nz])).pin_memory()
+               for k in ("rho", "sx", "sy", "sz", "E")}
+    p = grid.U_PAD
+    host_out = torch.empty((9, slab.nz, slab.n, slab.n), dtype=torch.float64).pin_memory()
+    e2e_steps = max(1, args.steps)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for v, k in enumerate(("rho", "sx", "sy", "sz", "E")):
+            u.U[v, p:p + slab.nz, p:p + slab.n, p:p + slab.n].copy_(host_in[k], non_blocking=True)
+        u.step()
+        host_out[:5].copy_(u.U[:, p:p + slab.nz, p:p + slab.n, p:p + slab.n], non_blocking=True)
+        host_out[5:].copy_(u.grav, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = t.item()
+    cells = slab.nz * slab.n * slab.n
+    h2d = 5 * cells * 8 * world
+    d2h = 9 * cells * 8 * world
+
+    m2l = per_kernel.get("m2l", {})
+    m2l_ms = m2l.get("mean_ms", float("nan"))
+    achieved = M2L_FLOP[1] * u.nleaves / (m2l_ms * 1e-3) / 1e12
+    roofline = {"kernel": "m2l", "bound": "fp64", "achieved": achieved, "unit": "TFLOP/s",
+                "peak": peaks["dfma_tflops"], "frac": achieved / peaks["dfma_tflops"],
+                "peak_source": "measured in this run: DFMA microbenchmark (sg_fp64_peak); FMA counted as 2 FLOP",
+                "peak_issue": peaks["dadd_tflops"], "frac_issue": achieved / peaks["dadd_tflops"],
+                "flop_per_subgrid": M2L_FLOP[1], "subgrids_per_launch": u.nleaves,
+                "traffic": None}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic config-5 IC (seedless, deterministic)",
+        "config": config_dict(world),
+        "e2e": {"value": total_leaves * e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "per_kernel": per_kernel,
+        "roofline": roofline,
+    }
+    if rank == 0:
+        line["clocks"] = clk.summary()
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            from oracle import oracle as O
+            kind = "port-native" if O.use_native() else "port"
+            threads = O.max_threads()
+            r = cpu_sample(state, LEVEL, threads, max(2 * threads, 32))
+            line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
+                                    "build": kind, "sample": r["sample"], "rates": r["rates"]}
+        except Exception as exc:  # the baseline is a report, never the product
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                                    "sample": f"failed: {exc}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

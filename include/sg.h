@@ -1,0 +1,146 @@
+/*
+ * sg.h -- C ABI of the B200-native (sm_100a) FP64 subgrid kernels (libsg.so).
+ *
+ * Drop-in boundary for the reference package's kernel layer
+ * (reference pkg/src/simdgrid/kernels/compiled.py: the seven numba array
+ * kernels).  Every entry point is a batched, stream-ordered mirror of one
+ * reference array kernel: plain device pointers, sizes and a cudaStream_t
+ * passed as void*; no torch or framework types.  The Python front end
+ * (paper_2210_06439_b200/kernels.py) mirrors the reference's Python entry
+ * points (kernels/__init__.py:122-267) on top of this ABI; INTEGRATION.md
+ * shows the ctypes binding a reference maintainer would add.
+ *
+ * Conventions
+ *  - Return value: SG_OK (0) or an error code; sg_last_error() gives a
+ *    thread-local message.  Launches are asynchronous on `stream`.
+ *  - Re-entrant: no global mutable state besides read-only constant tables;
+ *    concurrent calls on distinct outputs (e.g. one stream per caller) are safe.
+ *  - Field views.  A "view" of a cell-centred field is (base, nx, ny, nz, pad,
+ *    leaf_stride): `ncomp` components, each a C-contiguous array of dims
+ *    (nz+2*pad, ny+2*pad, nx+2*pad) indexed [z][y][x], component stride =
+ *    that volume.  Leaf b's interior starts at (pad + 8*cz, pad + 8*cy,
+ *    pad + 8*cx) of block b (address base + b*leaf_stride), where (cx,cy,cz)
+ *    = leaves[3b..3b+2] (int32, device) or (0,0,0) when leaves == NULL.
+ *      batched path : one global padded field, leaf_stride 0, leaf coords;
+ *      drop-in path : a stack of per-subgrid blocks, leaf_stride = block
+ *                     volume * ncomp, leaves == NULL.
+ *  - Arithmetic is FP64, IEEE round-to-nearest, no FMA contraction, the
+ *    reference's association and accumulation order: bit-identical results.
+ */
+#ifndef SG_H
+#define SG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_ABI_VERSION 1
+
+#define SG_OK 0
+#define SG_EINVAL 1
+#define SG_ECUDA 2
+
+int sg_abi_version(void);
+const char *sg_last_error(void);
+int sg_device_sm_count(void);
+
+/* ---------------------------------------------------------------- gravity */
+
+/* Replaces compiled.cluster_aggregate (compiled.py:324-352).
+ * mass: `nleaf` stacked C-contiguous arrays of dims (mnz, mny, mnx) (all
+ * even); clusters: matching (mnz/2, mny/2, mnx/2, 4) arrays of
+ * {M, Dx, Dy, Dz}.  Run on a whole padded global mass field (nleaf = 1) the
+ * result is bitwise equal to the reference's per-neighbourhood aggregation. */
+int sg_cluster_aggregate(const double *mass, int64_t mnx, int64_t mny, int64_t mnz, int64_t nleaf,
+                         double dx, double *clusters, void *stream);
+
+/* Replaces compiled.monopole_kernel_impl (compiled.py:281-321) called by
+ * kernels.monopole_kernel (kernels/__init__.py:205-221).
+ * mass view (pad >= halo), halo = gravity_halo(theta) <= 8; rad2 and eps2
+ * computed as kernels/__init__.py:215-218.  out view: 4 components
+ * (phi, gx, gy, gz), pad 0, dims (onx, ony, onz). */
+int sg_p2p(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+           const int32_t *leaves, int64_t nleaves, double dx, double rad2, double eps2, int32_t halo,
+           double *out, int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, void *stream);
+
+/* Replaces compiled.multipole_kernel_impl (compiled.py:355-451) called by
+ * kernels.multipole_prepare/multipole_kernel (kernels/__init__.py:224-261).
+ * mass view with even pad >= 8 (near-field cells), clusters from
+ * sg_cluster_aggregate over the same padded array (cluster_leaf_stride in
+ * doubles for stacked blocks, else 0), order in {0,1}, flat interior target
+ * range [i0, i1) (the reference's run(i0, i1) chunk), out view as sg_p2p. */
+int sg_m2l(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+           const double *clusters, int64_t cluster_leaf_stride, const int32_t *leaves, int64_t nleaves,
+           double dx, double rad2, double eps2, int32_t order, int32_t i0, int32_t i1, double *out,
+           int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, void *stream);
+
+/* ------------------------------------------------------------------ hydro */
+
+/* Replaces compiled.reconstruct_kernel (compiled.py:31-102) called by
+ * kernels.reconstruct (kernels/__init__.py:122-136).  U view: 5 components
+ * (rho, sx, sy, sz, E), pad >= 2 with ghosts filled.  Q: [nleaves][5][26][10][10][10]. */
+int sg_reconstruct(const double *U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+                   const int32_t *leaves, int64_t nleaves, double floor_, double *Q, void *stream);
+
+/* Replaces compiled.flux_kernel (compiled.py:105-262) called by kernels.flux
+ * (kernels/__init__.py:150-162).  FX [B][5][8][8][9], FY [B][5][8][9][8],
+ * FZ [B][5][9][8][8], smax[B]; err[B] = 0xFFFFFFFF or the reference's first
+ * error in loop order packed as key<<12 | code<<10 | cell (code 1 density,
+ * 2 pressure; cell = (z*10+y)*10+x in Q coordinates).  latch (nullable):
+ * latch[b] = min(latch[b], err[b]) so multi-iteration device runs can be
+ * checked once. */
+int sg_flux(const double *Q, int64_t nleaves, double gamma, double *FX, double *FY, double *FZ,
+            double *smax, uint32_t *err, uint32_t *latch, void *stream);
+
+/* Replaces compiled.hydro_update_kernel (compiled.py:265-278) plus the checks
+ * of kernels.hydro_update (kernels/__init__.py:165-188), in place on the U
+ * view.  dt from *dt_dev when non-NULL (device-computed, graph-capturable),
+ * else `dt`; dtdx = dt/dx on device.  smax (flux max speed) may be NULL to
+ * skip the CFL check.  status[b] = 0xFFFFFFFF ok, else kind<<16 | detail:
+ * kind 0 dt<=0, 1 CFL violation, 2 rho<=0/NaN at interior cell detail,
+ * 3 E<=0/NaN at cell detail (first in (z,y,x) order, rho before E).
+ * latch (nullable) as for sg_flux. */
+int sg_hydro_update(double *U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+                    const int32_t *leaves, int64_t nleaves, const double *FX, const double *FY,
+                    const double *FZ, const double *smax, const double *dt_dev, double dt, double dx,
+                    double cfl, uint32_t *status, uint32_t *latch, void *stream);
+
+/* Replaces compiled.max_wavespeed_kernel (compiled.py:454-480) called by
+ * kernels.max_wavespeed (kernels/__init__.py:264-267): smax[b] per leaf. */
+int sg_max_wavespeed(const double *U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+                     const int32_t *leaves, int64_t nleaves, double gamma, double pfloor, double *smax,
+                     void *stream);
+
+/* driver.py:170-171: s_pre = max over leaves (values >= 0), then
+ * dt = cfl*dx/(3*s_pre), both on device. */
+int sg_max_reduce(const double *vals, int64_t n, double *out, void *stream);
+int sg_dt_from_smax(const double *s_pre, double cfl, double dx, double *dt, void *stream);
+
+/* ------------------------------------------------------------------- grid */
+
+/* octree.exchange_ghosts / source_cube on a device-resident padded global
+ * field (octree.py:149-214): fill pad cells of `ncomp` components from the
+ * periodic image along the axes in wrap_mask (bit0 x, bit1 y, bit2 z).  In
+ * z-slab mode (wrap_mask = 3) z-halo planes come from the neighbour ranks
+ * and only their x/y pads are filled here. */
+int sg_fill_periodic(double *field, int64_t ncomp, int64_t nx, int64_t ny, int64_t nz, int32_t pad,
+                     int32_t wrap_mask, void *stream);
+
+/* driver.py:165-166: dst interior (pad dst_pad) = src component 0 interior
+ * (pad src_pad) * scale, with scale = dx**3. */
+int sg_scale_copy(double *dst, int32_t dst_pad, const double *src, int32_t src_pad, int64_t nx, int64_t ny,
+                  int64_t nz, double scale, void *stream);
+
+/* ------------------------------------------------------------ measurement */
+
+/* FP64 pipe microbenchmark (roofline denominator): mode 0 DFMA chains,
+ * mode 1 DADD chains; *flops_out = FLOPs issued (DFMA counted as 2). */
+int sg_fp64_peak(int mode, int iters, double *sink, int64_t *flops_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SG_H */

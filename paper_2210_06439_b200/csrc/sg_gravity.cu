@@ -1,0 +1,447 @@
+// Gravity kernels for sm_100a: cluster aggregation, P2P monopole, M2L
+// multipole.  FP64 CUDA cores only (the stencil interaction is not a dense
+// contraction; FP64 tensor-core throughput is not the bound here), one CTA
+// per 8^3 subgrid, one thread per target cell, persistent over the batch.
+//
+// Reference semantics (bit-exact):
+//   cluster_aggregate      compiled.py:324-352
+//   monopole_kernel_impl   compiled.py:281-321   (entry kernels/__init__.py:205-221)
+//   multipole_kernel_impl  compiled.py:355-451   (entry kernels/__init__.py:224-261)
+//
+// Data-independent geometry (r, r^2, sqrt, 1/r~, r~^-3, r~^-5 -- functions of
+// the offset, dx and eps only) is evaluated ONCE per CTA into shared-memory
+// tables with exactly the reference's expressions, so the per-pair loops run
+// only the data-dependent DADD/DMUL stream.  Masked (+0.0) terms and the
+// unselected far/near branch are skipped: accumulators start at +0.0 and are
+// never -0.0, so skipping x + 0.0 is exact.
+#include "sg_common.cuh"
+#include "../../include/sg.h"
+
+namespace sg {
+
+// ---------------------------------------------------------------------------
+// cluster aggregation over a whole (even-sized) mass array
+// ---------------------------------------------------------------------------
+__global__ void cluster_aggregate_kernel(const double* __restrict__ mass, int64_t mnx, int64_t mny,
+                                         int64_t ncx, int64_t ncy, int64_t ncz, double dx,
+                                         double4* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = ncx * ncy * ncz;
+    if (i >= total) return;
+    int64_t cx = i % ncx, cy = (i / ncx) % ncy, cz = i / (ncx * ncy);
+    double m_tot = 0.0, dxa = 0.0, dya = 0.0, dza = 0.0;
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+        const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+        const double m = __ldg(mass + ((2 * cz + oz) * mny + (2 * cy + oy)) * mnx + (2 * cx + ox));
+        m_tot = add(m_tot, m);
+        dxa = add(dxa, mul(m, mul(sub((double)ox, 0.5), dx)));
+        dya = add(dya, mul(m, mul(sub((double)oy, 0.5), dx)));
+        dza = add(dza, mul(m, mul(sub((double)oz, 0.5), dx)));
+    }
+    out[i] = make_double4(m_tot, dxa, dya, dza);
+}
+
+// ---------------------------------------------------------------------------
+// P2P monopole: radius-limited softened direct sum over the (8+2h)^3 cube
+// ---------------------------------------------------------------------------
+struct P2PEntry {
+    double rx, ry, rz, inv, inv3;
+    int32_t delta;  // source offset relative to the target, in smem cube cells
+    int32_t pad_;
+};
+
+constexpr int P2P_THREADS = 512;
+
+__host__ __device__ inline int p2p_pitch(int S) {
+    // row pitch (doubles) == 8 (mod 16): the two y-rows of a half-warp land on
+    // disjoint bank halves -> conflict-free 64-bit loads
+    int p = S;
+    while (p % 16 != 8) ++p;
+    return p;
+}
+
+// Build entries [c0, c0+512) of the lexicographic (oz, oy, ox) offset list,
+// compacted to the in-radius non-self ones, order preserved.  Returns count.
+__device__ int p2p_build_chunk(P2PEntry* ent, int* warp_cnt, int c0, int halo, double dx,
+                               double rad2, double eps2, int pitch, int plane) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int side = 2 * halo + 1;
+    const int total = side * side * side;
+    const int o = c0 + tid;
+    bool ok = false;
+    P2PEntry e;
+    if (o < total) {
+        const int ox = o % side - halo, oy = (o / side) % side - halo, oz = o / (side * side) - halo;
+        // compiled.py:299-313, same expression tree
+        const double rz = mul(-(double)oz, dx);
+        const double ry = mul(-(double)oy, dx);
+        const double rx = mul(-(double)ox, dx);
+        const double r2 = add(add(mul(rx, rx), mul(ry, ry)), mul(rz, rz));
+        ok = r2 <= rad2 && !(ox == 0 && oy == 0 && oz == 0);
+        if (ok) {
+            const double rt = dsqrt(add(r2, eps2));
+            const double inv = dvd(1.0, rt);
+            e.rx = rx;
+            e.ry = ry;
+            e.rz = rz;
+            e.inv = inv;
+            e.inv3 = mul(mul(inv, inv), inv);
+            e.delta = oz * plane + oy * pitch + ox;
+            e.pad_ = 0;
+        }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    if (lane == 0) warp_cnt[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, cnt = 0;
+    for (int w = 0; w < P2P_THREADS / 32; ++w) {
+        const int c = warp_cnt[w];
+        before += (w < warp) ? c : 0;
+        cnt += c;
+    }
+    if (ok) ent[before + __popc(bal & ((1u << lane) - 1u))] = e;
+    __syncthreads();
+    return cnt;
+}
+
+__global__ void __launch_bounds__(P2P_THREADS, 1)
+p2p_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, double dx, double rad2,
+           double eps2, int halo, FieldView ov, double* __restrict__ out_base) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int S = NIN + 2 * halo;
+    const int pitch = p2p_pitch(S);
+    const int plane = pitch * S;
+    P2PEntry* ent = reinterpret_cast<P2PEntry*>(smem_raw);
+    int* warp_cnt = reinterpret_cast<int*>(ent + P2P_THREADS);
+    double* cube = reinterpret_cast<double*>(warp_cnt + 32);
+
+    const int tid = threadIdx.x;
+    const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;
+    const int side = 2 * halo + 1;
+    const int total = side * side * side;
+    const bool single_chunk = total <= P2P_THREADS;
+    int count = 0;
+    if (single_chunk) count = p2p_build_chunk(ent, warp_cnt, 0, halo, dx, rad2, eps2, pitch, plane);
+    const int tcell = (z + halo) * plane + (y + halo) * pitch + (x + halo);
+
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        __syncthreads();
+        const double* src = leaf_origin(mv, leaves, b, halo);
+        for (int i = tid; i < S * S * S; i += P2P_THREADS) {
+            const int cx = i % S, cy = (i / S) % S, cz = i / (S * S);
+            cube[cz * plane + cy * pitch + cx] = __ldg(src + cz * mv.sz + cy * mv.sy + cx);
+        }
+        __syncthreads();
+        double acc_p = 0.0, acc_x = 0.0, acc_y = 0.0, acc_z = 0.0;
+        for (int c0 = 0; c0 < total; c0 += P2P_THREADS) {
+            if (!single_chunk) {
+                __syncthreads();
+                count = p2p_build_chunk(ent, warp_cnt, c0, halo, dx, rad2, eps2, pitch, plane);
+            }
+#pragma unroll 4
+            for (int e = 0; e < count; ++e) {
+                const P2PEntry& en = ent[e];
+                const double m = cube[tcell + en.delta];
+                const double pt = -mul(m, en.inv);
+                const double com = mul(m, en.inv3);
+                acc_p = add(acc_p, pt);
+                acc_x = add(acc_x, -mul(com, en.rx));
+                acc_y = add(acc_y, -mul(com, en.ry));
+                acc_z = add(acc_z, -mul(com, en.rz));
+            }
+        }
+        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy + x;
+        o[0] = acc_p;
+        o[ov.comp_stride] = acc_x;
+        o[2 * ov.comp_stride] = acc_y;
+        o[3 * ov.comp_stride] = acc_z;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// M2L multipole: 12^3 clusters per target, far = cluster expansion, near =
+// 8-cell direct sum.  One CTA per subgrid, 512 threads = 512 targets.
+// ---------------------------------------------------------------------------
+constexpr int M2L_THREADS = 512;
+constexpr int NC = 12;          // clusters per axis
+constexpr int TAB_N = 15;       // |k| - 1/2 in 0..14 per axis
+constexpr int TAB_PITCH = 56;   // [inv x16 | inv3 x16 | inv5 x16 | pad 8]: 112 words == 16 mod 32
+constexpr int NEAR_R = 4;       // near-cell table covers |s| in 0..3
+constexpr size_t M2L_SMEM = sizeof(double) * TAB_N * TAB_N * TAB_PITCH +
+                            sizeof(double2) * NEAR_R * NEAR_R * NEAR_R + sizeof(double4) * NC * NC * NC;
+
+struct ClusterView {
+    const double4* base;
+    int64_t sy, sz, leaf_stride;
+    int32_t off;  // cluster index of the cube origin for leaf (0,0,0)
+};
+
+__device__ __forceinline__ int fold(int v) { return v ^ (v >> 31); }  // v>=0 ? v : -v-1
+
+// near-field contribution of cluster (cz,cy,cx) for target (x,y,z):
+// compiled.py:419-442, same order (oz, oy, ox), self term masked.
+__device__ __noinline__ void m2l_near(const double* __restrict__ mc, int64_t msy, int64_t msz,
+                                      const double2* __restrict__ near_tab, int x, int y, int z,
+                                      int cx, int cy, int cz, double dx, double eps2, double* res) {
+    const double tx = (double)x + 0.5, ty = (double)y + 0.5, tz = (double)z + 0.5;
+    const double bx = (double)(2 * cx - 8), by = (double)(2 * cy - 8), bz = (double)(2 * cz - 8);
+    double p_n = 0.0, gx_n = 0.0, gy_n = 0.0, gz_n = 0.0;
+    const double* base = mc + (int64_t)(2 * cz) * msz + (int64_t)(2 * cy) * msy + 2 * cx;
+#pragma unroll 1
+    for (int o = 0; o < 8; ++o) {
+        const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+        const double m = __ldg(base + oz * msz + oy * msy + ox);
+        const double sx = mul(sub(tx, add(add(bx, (double)ox), 0.5)), dx);
+        const double sy = mul(sub(ty, add(add(by, (double)oy), 0.5)), dx);
+        const double sz = mul(sub(tz, add(add(bz, (double)oz), 0.5)), dx);
+        const int ix = abs(x - (2 * cx - 8 + ox)), iy = abs(y - (2 * cy - 8 + oy)), iz = abs(z - (2 * cz - 8 + oz));
+        double invs, invs3;
+        bool ok;
+        if (ix < NEAR_R && iy < NEAR_R && iz < NEAR_R) {
+            const double2 t = near_tab[(iz * NEAR_R + iy) * NEAR_R + ix];
+            ok = !signbit_d(t.x);
+            invs = t.x;
+            invs3 = t.y;
+        } else {
+            const double r2s = add(add(mul(sx, sx), mul(sy, sy)), mul(sz, sz));
+            ok = r2s > 0.0;
+            invs = dvd(1.0, dsqrt(add(r2s, eps2)));
+            invs3 = mul(mul(invs, invs), invs);
+        }
+        if (ok) {
+            const double coms = mul(m, invs3);
+            p_n = add(p_n, -mul(m, invs));
+            gx_n = add(gx_n, -mul(coms, sx));
+            gy_n = add(gy_n, -mul(coms, sy));
+            gz_n = add(gz_n, -mul(coms, sz));
+        }
+    }
+    res[0] = p_n;
+    res[1] = gx_n;
+    res[2] = gy_n;
+    res[3] = gz_n;
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(M2L_THREADS, 1)
+m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int64_t B, double dx,
+           double rad2, double eps2, int i0, int i1, FieldView ov) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* tab = reinterpret_cast<double*>(smem_raw);
+    double2* near_tab = reinterpret_cast<double2*>(tab + TAB_N * TAB_N * TAB_PITCH);
+    double4* cl = reinterpret_cast<double4*>(near_tab + NEAR_R * NEAR_R * NEAR_R);
+    const int tid = threadIdx.x;
+
+    // -- far geometry table, keyed by (|kx|,|ky|,|kz|) - 1/2 (compiled.py:394-414)
+    for (int e = tid; e < TAB_N * TAB_N * TAB_N; e += M2L_THREADS) {
+        const int ax = e % TAB_N, ay = (e / TAB_N) % TAB_N, az = e / (TAB_N * TAB_N);
+        // |t - (b + 1)| = a + 1/2 exactly; RN is sign-symmetric so |r| = (a+1/2)*dx
+        const double rx = mul(add((double)ax, 0.5), dx);
+        const double ry = mul(add((double)ay, 0.5), dx);
+        const double rz = mul(add((double)az, 0.5), dx);
+        const double r2 = add(add(mul(rx, rx), mul(ry, ry)), mul(rz, rz));
+        double* row = tab + (az * TAB_N + ay) * TAB_PITCH;
+        if (r2 > rad2) {
+            const double inv = dvd(1.0, dsqrt(add(r2, eps2)));
+            const double inv3 = mul(mul(inv, inv), inv);
+            row[ax] = inv;
+            row[16 + ax] = inv3;
+            row[32 + ax] = mul(mul(inv3, inv), inv);
+        } else {
+            row[ax] = -1.0;  // near marker (sign bit); near path computes its own terms
+            row[16 + ax] = 0.0;
+            row[32 + ax] = 0.0;
+        }
+    }
+    // -- near-cell table keyed by integer |s| per axis (compiled.py:429-438)
+    if (tid < NEAR_R * NEAR_R * NEAR_R) {
+        const int ix = tid % NEAR_R, iy = (tid / NEAR_R) % NEAR_R, iz = tid / (NEAR_R * NEAR_R);
+        const double sx = mul((double)ix, dx), sy = mul((double)iy, dx), sz = mul((double)iz, dx);
+        const double r2s = add(add(mul(sx, sx), mul(sy, sy)), mul(sz, sz));
+        if (r2s > 0.0) {
+            const double invs = dvd(1.0, dsqrt(add(r2s, eps2)));
+            near_tab[tid] = make_double2(invs, mul(mul(invs, invs), invs));
+        } else {
+            near_tab[tid] = make_double2(-1.0, 0.0);
+        }
+    }
+
+    const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;
+    const int f = (z * 8 + y) * 8 + x;
+    const bool active = f >= i0 && f < i1;
+    const double tx = (double)x + 0.5, ty = (double)y + 0.5, tz = (double)z + 0.5;
+    double rxv[NC];
+    int axv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const double bx = (double)(2 * c - 8);
+        rxv[c] = mul(sub(tx, add(bx, 1.0)), dx);  // compiled.py:394
+        axv[c] = fold(x - 2 * c + 7);
+    }
+
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        __syncthreads();
+        {  // stage this leaf's 12^3 clusters
+            int64_t cx0 = cv.off, cy0 = cv.off, cz0 = cv.off;
+            if (leaves) {
+                cx0 += 4 * (int64_t)leaves[3 * b];
+                cy0 += 4 * (int64_t)leaves[3 * b + 1];
+                cz0 += 4 * (int64_t)leaves[3 * b + 2];
+            }
+            const double4* src = cv.base + b * cv.leaf_stride + cz0 * cv.sz + cy0 * cv.sy + cx0;
+            for (int i = tid; i < NC * NC * NC; i += M2L_THREADS) {
+                const int cx = i % NC, cy = (i / NC) % NC, cz = i / (NC * NC);
+                const double2* s2 = reinterpret_cast<const double2*>(src + cz * cv.sz + cy * cv.sy + cx);
+                const double2 a = __ldg(s2), c2 = __ldg(s2 + 1);
+                cl[i] = make_double4(a.x, a.y, c2.x, c2.y);
+            }
+        }
+        __syncthreads();
+        if (!active) continue;
+        const double* mc = leaf_origin(mv, leaves, b, 8);
+        double acc_p = 0.0, acc_x = 0.0, acc_y = 0.0, acc_z = 0.0;
+#pragma unroll 1
+        for (int cz = 0; cz < NC; ++cz) {
+            const double rz = mul(sub(tz, add((double)(2 * cz - 8), 1.0)), dx);
+            const int az = fold(z - 2 * cz + 7);
+#pragma unroll 1
+            for (int cy = 0; cy < NC; ++cy) {
+                const double ry = mul(sub(ty, add((double)(2 * cy - 8), 1.0)), dx);
+                const int ay = fold(y - 2 * cy + 7);
+                const double* row = tab + (az * TAB_N + ay) * TAB_PITCH;
+                const double4* crow = cl + (cz * NC + cy) * NC;
+#pragma unroll
+                for (int cx = 0; cx < NC; ++cx) {
+                    const double inv = row[axv[cx]];
+                    const double rx = rxv[cx];
+                    if (!signbit_d(inv)) {
+                        // far: compiled.py:399-418
+                        const double inv3 = row[16 + axv[cx]];
+                        const double4 c = crow[cx];
+                        double p_f = -mul(c.x, inv);
+                        const double gcom = mul(c.x, inv3);
+                        double gx_f = -mul(gcom, rx);
+                        double gy_f = -mul(gcom, ry);
+                        double gz_f = -mul(gcom, rz);
+                        if (ORDER == 1) {
+                            const double inv5 = row[32 + axv[cx]];
+                            const double dr = add(add(mul(c.y, rx), mul(c.z, ry)), mul(c.w, rz));
+                            p_f = sub(p_f, mul(dr, inv3));
+                            const double t3 = mul(mul(3.0, dr), inv5);
+                            gx_f = sub(add(gx_f, mul(c.y, inv3)), mul(t3, rx));
+                            gy_f = sub(add(gy_f, mul(c.z, inv3)), mul(t3, ry));
+                            gz_f = sub(add(gz_f, mul(c.w, inv3)), mul(t3, rz));
+                        }
+                        acc_p = add(acc_p, p_f);
+                        acc_x = add(acc_x, gx_f);
+                        acc_y = add(acc_y, gy_f);
+                        acc_z = add(acc_z, gz_f);
+                    } else {
+                        double r[4];
+                        m2l_near(mc, mv.sy, mv.sz, near_tab, x, y, z, cx, cy, cz, dx, eps2, r);
+                        acc_p = add(acc_p, r[0]);
+                        acc_x = add(acc_x, r[1]);
+                        acc_y = add(acc_y, r[2]);
+                        acc_z = add(acc_z, r[3]);
+                    }
+                }
+            }
+        }
+        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy + x;
+        o[0] = acc_p;
+        o[ov.comp_stride] = acc_x;
+        o[2 * ov.comp_stride] = acc_y;
+        o[3 * ov.comp_stride] = acc_z;
+    }
+}
+
+static int g_sm_count = 0;
+int sm_count() {
+    if (g_sm_count == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sm_count <= 0) g_sm_count = 148;
+    }
+    return g_sm_count;
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+int sg_cluster_aggregate(const double* mass, int64_t mnx, int64_t mny, int64_t mnz, int64_t nleaf,
+                         double dx, double* clusters, void* stream) {
+    if ((mnx | mny | mnz) & 1) {
+        sg_set_error("sg_cluster_aggregate: mass dims must be even (got %lld,%lld,%lld)",
+                     (long long)mnx, (long long)mny, (long long)mnz);
+        return SG_EINVAL;
+    }
+    if (nleaf < 1) nleaf = 1;
+    const int64_t ncx = mnx / 2, ncy = mny / 2, ncz = mnz / 2;
+    const int64_t total = ncx * ncy * ncz * nleaf;
+    if (total == 0) return SG_OK;
+    // stacked blocks are contiguous, so treat them as one taller array
+    cluster_aggregate_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        mass, mnx, mny, ncx, ncy, ncz * nleaf, dx, reinterpret_cast<double4*>(clusters));
+    return sg_check_launch("sg_cluster_aggregate");
+}
+
+int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+           const int32_t* leaves, int64_t nleaves, double dx, double rad2, double eps2, int32_t halo,
+           double* out, int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, void* stream) {
+    if (halo < 0 || halo > 8 || halo > pad) {
+        sg_set_error("sg_p2p: halo %d must be in [0, min(8, pad=%d)]", halo, pad);
+        return SG_EINVAL;
+    }
+    if (nleaves <= 0) return SG_OK;
+    FieldView mv = make_view(mass, nx, ny, nz, pad, leaf_stride);
+    FieldView ov = make_view(out, onx, ony, onz, 0, out_leaf_stride);
+    const int S = NIN + 2 * halo;
+    const size_t smem = sizeof(P2PEntry) * P2P_THREADS + sizeof(int) * 32 +
+                        sizeof(double) * (size_t)S * S * p2p_pitch(S);
+    cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t grid = nleaves < 2 * sm_count() ? nleaves : 2 * sm_count();
+    p2p_kernel<<<(unsigned)grid, P2P_THREADS, smem, (cudaStream_t)stream>>>(
+        mv, leaves, nleaves, dx, rad2, eps2, halo, ov, out);
+    return sg_check_launch("sg_p2p");
+}
+
+int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+           const double* clusters, int64_t cluster_leaf_stride, const int32_t* leaves, int64_t nleaves,
+           double dx, double rad2, double eps2, int32_t order, int32_t i0, int32_t i1, double* out,
+           int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, void* stream) {
+    if (pad < 8 || (pad & 1)) {
+        sg_set_error("sg_m2l: mass pad must be even and >= 8 (got %d)", pad);
+        return SG_EINVAL;
+    }
+    if (order != 0 && order != 1) {
+        sg_set_error("sg_m2l: expansion order must be 0 or 1 (got %d)", order);
+        return SG_EINVAL;
+    }
+    if (nleaves <= 0 || i1 <= i0) return SG_OK;
+    FieldView mv = make_view(mass, nx, ny, nz, pad, leaf_stride);
+    ClusterView cv;
+    cv.base = reinterpret_cast<const double4*>(clusters);
+    cv.sy = (nx + 2 * pad) / 2;
+    cv.sz = cv.sy * ((ny + 2 * pad) / 2);
+    cv.leaf_stride = cluster_leaf_stride / 4;
+    cv.off = (pad - 8) / 2;
+    FieldView ov = make_view(out, onx, ony, onz, 0, out_leaf_stride);
+    const int64_t grid = nleaves < sm_count() ? nleaves : sm_count();
+    if (order == 1) {
+        cudaFuncSetAttribute(m2l_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M2L_SMEM);
+        m2l_kernel<1><<<(unsigned)grid, M2L_THREADS, M2L_SMEM, (cudaStream_t)stream>>>(
+            mv, cv, leaves, nleaves, dx, rad2, eps2, i0, i1, ov);
+    } else {
+        cudaFuncSetAttribute(m2l_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M2L_SMEM);
+        m2l_kernel<0><<<(unsigned)grid, M2L_THREADS, M2L_SMEM, (cudaStream_t)stream>>>(
+            mv, cv, leaves, nleaves, dx, rad2, eps2, i0, i1, ov);
+    }
+    return sg_check_launch("sg_m2l");
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// Device-resident grid plumbing: periodic ghost fill of padded global fields
+// (the batched replacement of octree.exchange_ghosts / source_cube,
+// reference octree.py:149-214), the per-step mass = rho*dx^3 copy
+// (driver.py:165-166), and error/status helpers shared by the C-ABI.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "sg_common.cuh"
+#include "../../include/sg.h"
+
+static thread_local char g_err[512] = "";
+
+void sg_set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int sg_check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        sg_set_error("%s: %s", what, cudaGetErrorString(e));
+        return SG_ECUDA;
+    }
+    return SG_OK;
+}
+
+namespace sg {
+
+// Fill the pad cells of `ncomp` padded fields (dims (nz+2p, ny+2p, nx+2p))
+// from the periodic image of the interior.  Axes not in wrap_mask (bit0 x,
+// bit1 y, bit2 z) are left untouched in their pad range: the z-slab halo
+// exchange fills those planes from the neighbouring rank.
+__global__ void fill_periodic_kernel(double* __restrict__ f, int64_t ncomp, int64_t nx, int64_t ny,
+                                     int64_t nz, int pad, int wrap_mask) {
+    const int64_t X = nx + 2 * pad, Y = ny + 2 * pad, Z = nz + 2 * pad;
+    const int64_t vol = X * Y * Z;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= vol * ncomp) return;
+    const int64_t c = i / vol, r = i % vol;
+    const int64_t x = r % X, y = (r / X) % Y, z = r / (X * Y);
+    const bool ix = x >= pad && x < pad + nx, iy = y >= pad && y < pad + ny, iz = z >= pad && z < pad + nz;
+    if (ix && iy && iz) return;
+    auto wrapc = [pad](int64_t v, int64_t n) {
+        int64_t w = (v - pad) % n;
+        if (w < 0) w += n;
+        return w + pad;
+    };
+    // wrapped axes map to their periodic image; a non-wrapped axis keeps its
+    // coordinate (its halo planes are filled externally, then their x/y pads
+    // are wrapped here within the same plane).  Sources are never pad cells
+    // of a wrapped axis, so the fill has no read/write overlap.
+    const int64_t sx = (!ix && (wrap_mask & 1)) ? wrapc(x, nx) : x;
+    const int64_t sy = (!iy && (wrap_mask & 2)) ? wrapc(y, ny) : y;
+    const int64_t sz = (!iz && (wrap_mask & 4)) ? wrapc(z, nz) : z;
+    if (sx == x && sy == y && sz == z) return;
+    f[i] = f[c * vol + (sz * Y + sy) * X + sx];
+}
+
+// dst interior (pad pd) = src interior (pad ps, component 0) * scale
+__global__ void scale_copy_kernel(double* __restrict__ dst, int pd, const double* __restrict__ src, int ps,
+                                  int64_t nx, int64_t ny, int64_t nz, double scale) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nx * ny * nz) return;
+    const int64_t x = i % nx, y = (i / nx) % ny, z = i / (nx * ny);
+    const int64_t Xd = nx + 2 * pd, Yd = ny + 2 * pd, Xs = nx + 2 * ps, Ys = ny + 2 * ps;
+    dst[((z + pd) * Yd + (y + pd)) * Xd + (x + pd)] = mul(src[((z + ps) * Ys + (y + ps)) * Xs + (x + ps)], scale);
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+int sg_abi_version(void) { return SG_ABI_VERSION; }
+
+const char* sg_last_error(void) { return g_err; }
+
+int sg_device_sm_count(void) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    return n;
+}
+
+int sg_fill_periodic(double* field, int64_t ncomp, int64_t nx, int64_t ny, int64_t nz, int32_t pad,
+                     int32_t wrap_mask, void* stream) {
+    if (pad < 0 || nx <= 0 || ny <= 0 || nz <= 0) {
+        sg_set_error("sg_fill_periodic: bad geometry pad=%d interior=(%lld,%lld,%lld)", pad,
+                     (long long)nx, (long long)ny, (long long)nz);
+        return SG_EINVAL;
+    }
+    const int64_t total = (nx + 2 * pad) * (ny + 2 * pad) * (nz + 2 * pad) * ncomp;
+    if (total == 0 || pad == 0) return SG_OK;
+    fill_periodic_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        field, ncomp, nx, ny, nz, pad, wrap_mask);
+    return sg_check_launch("sg_fill_periodic");
+}
+
+int sg_scale_copy(double* dst, int32_t dst_pad, const double* src, int32_t src_pad, int64_t nx, int64_t ny,
+                  int64_t nz, double scale, void* stream) {
+    const int64_t total = nx * ny * nz;
+    if (total == 0) return SG_OK;
+    scale_copy_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        dst, dst_pad, src, src_pad, nx, ny, nz, scale);
+    return sg_check_launch("sg_scale_copy");
+}
+
+}  // extern "C"

@@ -1,0 +1,418 @@
+// Hydro kernels for sm_100a: minmod reconstruction at the 26 lattice
+// directions, Rusanov flux with 3x3 Simpson face quadrature, forward-Euler
+// conservative update with the reference's validity checks, and the
+// cell-centred max wave speed with the dt reduction.
+//
+// Reference semantics (bit-exact):
+//   reconstruct_kernel     compiled.py:31-102    (entry kernels/__init__.py:122-136)
+//   flux_kernel            compiled.py:105-262   (entry kernels/__init__.py:150-162)
+//   hydro_update_kernel    compiled.py:265-278   (entry kernels/__init__.py:165-188)
+//   max_wavespeed_kernel   compiled.py:454-480   (entry kernels/__init__.py:264-267)
+//   dt = cfl*dx/(3*s_pre)  driver.py:170-171
+//
+// The unfused reconstruct -> Q -> flux pair is the drop-in path and is
+// HBM-bound (Q is 1.04 MB per subgrid).  Parallelism comes only from
+// independent outputs (cells, faces, subgrids); every per-output chain keeps
+// the reference's sequential order.
+#include "sg_common.cuh"
+#include "../../include/sg.h"
+
+namespace sg {
+
+// geometry.py:21-31: (dz, dy, dx) lexicographic without the zero offset
+__constant__ double c_dirs[NDIR][3];
+// geometry.py:41-56
+__constant__ int c_dplus[3][9];
+__constant__ int c_dminus[3][9];
+// geometry.py:59-61
+__constant__ double c_simpson[9];
+
+static bool g_tables_ready = false;
+
+static int host_dir_index(int dz, int dy, int dx) {
+    int idx = (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
+    return idx > 13 ? idx - 1 : idx;
+}
+
+static int init_tables() {
+    if (g_tables_ready) return SG_OK;
+    double dirs[NDIR][3];
+    int d = 0;
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                if (!dz && !dy && !dx) continue;
+                dirs[d][0] = dz;
+                dirs[d][1] = dy;
+                dirs[d][2] = dx;
+                ++d;
+            }
+    int dp[3][9], dm[3][9];
+    const int t[3] = {-1, 0, 1};
+    for (int i1 = 0; i1 < 3; ++i1)
+        for (int i2 = 0; i2 < 3; ++i2) {
+            const int t1 = t[i1], t2 = t[i2], q = i1 * 3 + i2;
+            dp[0][q] = host_dir_index(t2, t1, 1);
+            dm[0][q] = host_dir_index(t2, t1, -1);
+            dp[1][q] = host_dir_index(t2, 1, t1);
+            dm[1][q] = host_dir_index(t2, -1, t1);
+            dp[2][q] = host_dir_index(1, t2, t1);
+            dm[2][q] = host_dir_index(-1, t2, t1);
+        }
+    const double w[9] = {1.0, 4.0, 1.0, 4.0, 16.0, 4.0, 1.0, 4.0, 1.0};
+    double sw[9];
+    for (int i = 0; i < 9; ++i) sw[i] = w[i] / 36.0;  // host IEEE division, as numpy
+    if (cudaMemcpyToSymbol(c_dirs, dirs, sizeof(dirs)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_dplus, dp, sizeof(dp)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_dminus, dm, sizeof(dm)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_simpson, sw, sizeof(sw)) != cudaSuccess) {
+        sg_set_error("hydro constant tables: %s", cudaGetErrorString(cudaGetLastError()));
+        return SG_ECUDA;
+    }
+    g_tables_ready = true;
+    return SG_OK;
+}
+
+__device__ __forceinline__ double minmod(double ap, double am) {
+    // compiled.py:58-62 (select semantics, NaN-preserving)
+    const double mag = fabs(ap) < fabs(am) ? ap : am;
+    const bool sgn = (ap > 0.0 && am > 0.0) || (ap < 0.0 && am < 0.0);
+    return sgn ? mag : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// reconstruct: U view (5 comps, G=2 ghosts around each leaf) -> Q[B,5,26,10^3]
+// ---------------------------------------------------------------------------
+constexpr int REC_THREADS = 256;
+constexpr int REC_CELLS = NRC * NRC * NRC;
+
+__global__ void __launch_bounds__(REC_THREADS)
+reconstruct_kernel(FieldView uv, const int32_t* __restrict__ leaves, double floor_, double* __restrict__ Q) {
+    const int cell = blockIdx.x * REC_THREADS + threadIdx.x;
+    const int64_t b = blockIdx.y;
+    if (cell >= REC_CELLS) return;
+    const int x = cell % NRC, y = (cell / NRC) % NRC, z = cell / (NRC * NRC);
+    const double* u0 = leaf_origin(uv, leaves, b, 2) + (z + 1) * uv.sz + (y + 1) * uv.sy + (x + 1);
+    double uc[NVAR], sl[NVAR][3];
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) {
+        const double* p = u0 + v * uv.comp_stride;
+        const double u = __ldg(p);
+        uc[v] = u;
+        sl[v][0] = minmod(sub(__ldg(p + 1), u), sub(u, __ldg(p - 1)));
+        sl[v][1] = minmod(sub(__ldg(p + uv.sy), u), sub(u, __ldg(p - uv.sy)));
+        sl[v][2] = minmod(sub(__ldg(p + uv.sz), u), sub(u, __ldg(p - uv.sz)));
+    }
+    double* q = Q + b * (int64_t)(NVAR * NDIR * REC_CELLS) + cell;
+#pragma unroll 2
+    for (int d = 0; d < NDIR; ++d) {
+        const double fdz = c_dirs[d][0], fdy = c_dirs[d][1], fdx = c_dirs[d][2];
+        double r[NVAR];
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v)
+            r[v] = add(uc[v], mul(0.5, add(add(mul(fdx, sl[v][0]), mul(fdy, sl[v][1])), mul(fdz, sl[v][2]))));
+        double rho = r[0] < floor_ ? floor_ : r[0];
+        double en = r[4] < floor_ ? floor_ : r[4];
+        const double ke = dvd(mul(0.5, add(add(mul(r[1], r[1]), mul(r[2], r[2])), mul(r[3], r[3]))), rho);
+        const double emin = add(mul(ke, add(1.0, floor_)), floor_);
+        en = en < emin ? emin : en;
+        q[(0 * NDIR + d) * REC_CELLS] = rho;
+        q[(1 * NDIR + d) * REC_CELLS] = r[1];
+        q[(2 * NDIR + d) * REC_CELLS] = r[2];
+        q[(3 * NDIR + d) * REC_CELLS] = r[3];
+        q[(4 * NDIR + d) * REC_CELLS] = en;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// flux: Q -> FX[B,5,8,8,9], FY[B,5,8,9,8], FZ[B,5,9,8,8], smax[B], err[B]
+// err packs the reference's FIRST error in loop order:
+//   key = ((((axis*8+i)*9+j)*9+k)*9 + q)*4 + check ; err = key<<12 | code<<10 | cell
+// 0xFFFFFFFF = no error.
+// ---------------------------------------------------------------------------
+constexpr int FLUX_THREADS = 576;
+
+__global__ void __launch_bounds__(FLUX_THREADS)
+flux_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX, double* __restrict__ FY,
+            double* __restrict__ FZ, double* __restrict__ smax_out, uint32_t* __restrict__ err_out,
+            uint32_t* __restrict__ latch) {
+    __shared__ unsigned long long s_smax;
+    __shared__ uint32_t s_err;
+    const int64_t b = blockIdx.x;
+    const int t = threadIdx.x;
+    if (t == 0) {
+        s_smax = 0ull;  // +0.0
+        s_err = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    const double* Qb = Q + b * (int64_t)(NVAR * NDIR * REC_CELLS);
+    const double gm1 = sub(gamma, 1.0);
+    double smax = 0.0;
+    uint32_t err = 0xFFFFFFFFu;
+#pragma unroll 1
+    for (int axis = 0; axis < 3; ++axis) {
+        const int nj = axis == 0 ? NIN : NIN + 1;
+        const int nk = axis == 0 ? NIN + 1 : NIN;
+        const int k = t % nk, j = (t / nk) % nj, i = t / (nk * nj);
+        int zl, zr, yl, yr, xl, xr;
+        if (axis == 0) {
+            zl = zr = i + 1; yl = yr = j + 1; xl = k; xr = k + 1;
+        } else if (axis == 1) {
+            zl = zr = i + 1; yl = j; yr = j + 1; xl = xr = k + 1;
+        } else {
+            zl = j; zr = j + 1; yl = yr = i + 1; xl = xr = k + 1;
+        }
+        const int cl_ = (zl * NRC + yl) * NRC + xl, cr_ = (zr * NRC + yr) * NRC + xr;
+        const uint32_t kbase = (uint32_t)((((axis * 8 + i) * 9 + j) * 9 + k) * 9);
+        double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0, f4 = 0.0;
+#pragma unroll 1
+        for (int qp = 0; qp < 9; ++qp) {
+            const double w = c_simpson[qp];
+            const double* pl_ = Qb + c_dplus[axis][qp] * REC_CELLS + cl_;
+            const double* pr_ = Qb + c_dminus[axis][qp] * REC_CELLS + cr_;
+            const int64_t VS = (int64_t)NDIR * REC_CELLS;
+            const double ul0 = __ldg(pl_), ul1 = __ldg(pl_ + VS), ul2 = __ldg(pl_ + 2 * VS),
+                         ul3 = __ldg(pl_ + 3 * VS), ul4 = __ldg(pl_ + 4 * VS);
+            const double ur0 = __ldg(pr_), ur1 = __ldg(pr_ + VS), ur2 = __ldg(pr_ + 2 * VS),
+                         ur3 = __ldg(pr_ + 3 * VS), ur4 = __ldg(pr_ + 4 * VS);
+            const uint32_t key = (kbase + qp) * 4;
+            if (err == 0xFFFFFFFFu) {
+                if (ul0 <= 0.0) err = ((key + 0) << 12) | (1u << 10) | (uint32_t)cl_;
+                else if (ur0 <= 0.0) err = ((key + 1) << 12) | (1u << 10) | (uint32_t)cr_;
+            }
+            const double invl = dvd(1.0, ul0);
+            const double vxl = mul(ul1, invl), vyl = mul(ul2, invl), vzl = mul(ul3, invl);
+            const double kel = mul(0.5, add(add(mul(ul1, vxl), mul(ul2, vyl)), mul(ul3, vzl)));
+            const double pl = mul(gm1, sub(ul4, kel));
+            const double invr = dvd(1.0, ur0);
+            const double vxr = mul(ur1, invr), vyr = mul(ur2, invr), vzr = mul(ur3, invr);
+            const double ker = mul(0.5, add(add(mul(ur1, vxr), mul(ur2, vyr)), mul(ur3, vzr)));
+            const double pr = mul(gm1, sub(ur4, ker));
+            if (err == 0xFFFFFFFFu) {
+                if (pl <= 0.0) err = ((key + 2) << 12) | (2u << 10) | (uint32_t)cl_;
+                else if (pr <= 0.0) err = ((key + 3) << 12) | (2u << 10) | (uint32_t)cr_;
+            }
+            const double cl = dsqrt(mul(mul(gamma, pl), invl));
+            const double cr = dsqrt(mul(mul(gamma, pr), invr));
+            const double vnl = axis == 0 ? vxl : (axis == 1 ? vyl : vzl);
+            const double vnr = axis == 0 ? vxr : (axis == 1 ? vyr : vzr);
+            const double sl = add(fabs(vnl), cl);
+            const double sr = add(fabs(vnr), cr);
+            const double s = sl > sr ? sl : sr;
+            if (s > smax) smax = s;
+            const double fl0 = mul(ul0, vnl);
+            double fl1 = mul(ul1, vnl), fl2 = mul(ul2, vnl), fl3 = mul(ul3, vnl);
+            const double fl4 = mul(add(ul4, pl), vnl);
+            const double fr0 = mul(ur0, vnr);
+            double fr1 = mul(ur1, vnr), fr2 = mul(ur2, vnr), fr3 = mul(ur3, vnr);
+            const double fr4 = mul(add(ur4, pr), vnr);
+            if (axis == 0) {
+                fl1 = add(fl1, pl);
+                fr1 = add(fr1, pr);
+            } else if (axis == 1) {
+                fl2 = add(fl2, pl);
+                fr2 = add(fr2, pr);
+            } else {
+                fl3 = add(fl3, pl);
+                fr3 = add(fr3, pr);
+            }
+            const double hs = mul(0.5, s);
+            f0 = add(f0, mul(w, sub(mul(0.5, add(fl0, fr0)), mul(hs, sub(ur0, ul0)))));
+            f1 = add(f1, mul(w, sub(mul(0.5, add(fl1, fr1)), mul(hs, sub(ur1, ul1)))));
+            f2 = add(f2, mul(w, sub(mul(0.5, add(fl2, fr2)), mul(hs, sub(ur2, ul2)))));
+            f3 = add(f3, mul(w, sub(mul(0.5, add(fl3, fr3)), mul(hs, sub(ur3, ul3)))));
+            f4 = add(f4, mul(w, sub(mul(0.5, add(fl4, fr4)), mul(hs, sub(ur4, ul4)))));
+        }
+        double* F;
+        int64_t vs;
+        if (axis == 0) {
+            F = FX + b * 5 * 576 + (i * 8 + j) * 9 + k;
+            vs = 576;
+        } else if (axis == 1) {
+            F = FY + b * 5 * 576 + (i * 9 + j) * 8 + k;
+            vs = 576;
+        } else {
+            F = FZ + b * 5 * 576 + (j * 8 + i) * 8 + k;
+            vs = 576;
+        }
+        F[0] = f0;
+        F[vs] = f1;
+        F[2 * vs] = f2;
+        F[3 * vs] = f3;
+        F[4 * vs] = f4;
+    }
+    // smax >= 0 and never NaN: its bit pattern orders like an unsigned integer
+    atomicMax(&s_smax, (unsigned long long)__double_as_longlong(smax));
+    if (err != 0xFFFFFFFFu) atomicMin(&s_err, err);
+    __syncthreads();
+    if (t == 0) {
+        smax_out[b] = __longlong_as_double((long long)s_smax);
+        err_out[b] = s_err;
+        if (latch && s_err != 0xFFFFFFFFu) atomicMin(latch + b, s_err);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// hydro update (in place on the U view) + the reference's checks
+// (kernels/__init__.py:168-187):  status = 0xFFFFFFFF ok, else
+//   kind<<16 | detail,  kind 0: dt<=0, 1: CFL, 2: rho<=0/NaN at cell, 3: E
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512)
+hydro_update_kernel(FieldView uv, const int32_t* __restrict__ leaves, const double* __restrict__ FX,
+                    const double* __restrict__ FY, const double* __restrict__ FZ,
+                    const double* __restrict__ smax, const double* __restrict__ dt_dev, double dt_val,
+                    double dx, double cfl, uint32_t* __restrict__ status, uint32_t* __restrict__ latch) {
+    __shared__ uint32_t s_st;
+    const int64_t b = blockIdx.x;
+    const int t = threadIdx.x;
+    const double dt = dt_dev ? *dt_dev : dt_val;
+    if (t == 0) {
+        uint32_t st = 0xFFFFFFFFu;
+        if (!(dt > 0.0)) st = 0u << 16;
+        else if (smax && mul(dt, smax[b]) > mul(cfl, dx)) st = 1u << 16;
+        s_st = st;
+    }
+    __syncthreads();
+    const double dtdx = dvd(dt, dx);
+    const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+    double* u = const_cast<double*>(leaf_origin(uv, leaves, b, 0)) + z * uv.sz + y * uv.sy + x;
+    const double* fx = FX + b * 5 * 576 + (z * 8 + y) * 9 + x;
+    const double* fy = FY + b * 5 * 576 + (z * 9 + y) * 8 + x;
+    const double* fz = FZ + b * 5 * 576 + (z * 8 + y) * 8 + x;
+    double rho = 0.0, en = 0.0;
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) {
+        const int64_t o = v * 576;
+        const double net = add(add(sub(fx[o + 1], fx[o]), sub(fy[o + 8], fy[o])), sub(fz[o + 64], fz[o]));
+        const double nu = sub(u[v * uv.comp_stride], mul(dtdx, net));
+        u[v * uv.comp_stride] = nu;
+        if (v == 0) rho = nu;
+        if (v == 4) en = nu;
+    }
+    const int cell = (z * 8 + y) * 8 + x;
+    if (!(rho > 0.0)) atomicMin(&s_st, (2u << 16) | (uint32_t)cell);
+    else if (!(en > 0.0)) atomicMin(&s_st, (3u << 16) | (uint32_t)cell);
+    __syncthreads();
+    if (t == 0) {
+        if (status) status[b] = s_st;
+        if (latch && s_st != 0xFFFFFFFFu) atomicMin(latch + b, s_st);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// max wave speed per leaf (compiled.py:454-480) and the dt reduction
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512)
+max_wavespeed_kernel(FieldView uv, const int32_t* __restrict__ leaves, double gamma, double pfloor,
+                     double* __restrict__ out) {
+    __shared__ unsigned long long s_max;
+    const int64_t b = blockIdx.x;
+    const int t = threadIdx.x;
+    if (t == 0) s_max = 0ull;
+    __syncthreads();
+    const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+    const double* u = leaf_origin(uv, leaves, b, 0) + z * uv.sz + y * uv.sy + x;
+    const int64_t cs = uv.comp_stride;
+    const double gm1 = sub(gamma, 1.0);
+    const double rho = __ldg(u), m1 = __ldg(u + cs), m2 = __ldg(u + 2 * cs), m3 = __ldg(u + 3 * cs),
+                 e = __ldg(u + 4 * cs);
+    const double inv = dvd(1.0, rho);
+    const double vx = mul(m1, inv), vy = mul(m2, inv), vz = mul(m3, inv);
+    const double ke = mul(0.5, add(add(mul(m1, vx), mul(m2, vy)), mul(m3, vz)));
+    double p = mul(gm1, sub(e, ke));
+    if (!(p > pfloor)) p = pfloor;
+    const double c = dsqrt(mul(mul(gamma, p), inv));
+    double av = fabs(vx);
+    if (fabs(vy) > av) av = fabs(vy);
+    if (fabs(vz) > av) av = fabs(vz);
+    const double s = add(av, c);
+    // reference: `if s > smax: smax = s` from 0.0 -> max over non-NaN s >= 0
+    if (s > 0.0) atomicMax(&s_max, (unsigned long long)__double_as_longlong(s));
+    __syncthreads();
+    if (t == 0) out[b] = __longlong_as_double((long long)s_max);
+}
+
+__global__ void max_reduce_kernel(const double* __restrict__ vals, int64_t n, double* __restrict__ out) {
+    __shared__ unsigned long long s_max;
+    if (threadIdx.x == 0) s_max = 0ull;
+    __syncthreads();
+    double m = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = vals[i];
+        if (v > m) m = v;
+    }
+    atomicMax(&s_max, (unsigned long long)__double_as_longlong(m));
+    __syncthreads();
+    if (threadIdx.x == 0) *out = __longlong_as_double((long long)s_max);
+}
+
+__global__ void dt_kernel(const double* __restrict__ s_pre, double cfl, double dx, double* __restrict__ dt) {
+    // driver.py:171  dt = cfl * dx / (3.0 * s_pre)
+    *dt = dvd(mul(cfl, dx), mul(3.0, *s_pre));
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+int sg_reconstruct(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+                   const int32_t* leaves, int64_t nleaves, double floor_, double* Q, void* stream) {
+    if (pad < 2) {
+        sg_set_error("sg_reconstruct: U pad must be >= 2 (got %d)", pad);
+        return SG_EINVAL;
+    }
+    int rc = init_tables();
+    if (rc) return rc;
+    if (nleaves <= 0) return SG_OK;
+    if (nleaves > 65535) {
+        sg_set_error("sg_reconstruct: at most 65535 leaves per call (got %lld)", (long long)nleaves);
+        return SG_EINVAL;
+    }
+    FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
+    dim3 grid((REC_CELLS + REC_THREADS - 1) / REC_THREADS, (unsigned)nleaves);
+    reconstruct_kernel<<<grid, REC_THREADS, 0, (cudaStream_t)stream>>>(uv, leaves, floor_, Q);
+    return sg_check_launch("sg_reconstruct");
+}
+
+int sg_flux(const double* Q, int64_t nleaves, double gamma, double* FX, double* FY, double* FZ,
+            double* smax, uint32_t* err, uint32_t* latch, void* stream) {
+    int rc = init_tables();
+    if (rc) return rc;
+    if (nleaves <= 0) return SG_OK;
+    flux_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax, err, latch);
+    return sg_check_launch("sg_flux");
+}
+
+int sg_hydro_update(double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+                    const int32_t* leaves, int64_t nleaves, const double* FX, const double* FY,
+                    const double* FZ, const double* smax, const double* dt_dev, double dt, double dx,
+                    double cfl, uint32_t* status, uint32_t* latch, void* stream) {
+    if (nleaves <= 0) return SG_OK;
+    FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
+    hydro_update_kernel<<<(unsigned)nleaves, 512, 0, (cudaStream_t)stream>>>(
+        uv, leaves, FX, FY, FZ, smax, dt_dev, dt, dx, cfl, status, latch);
+    return sg_check_launch("sg_hydro_update");
+}
+
+int sg_max_wavespeed(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+                     const int32_t* leaves, int64_t nleaves, double gamma, double pfloor, double* smax,
+                     void* stream) {
+    if (nleaves <= 0) return SG_OK;
+    FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
+    max_wavespeed_kernel<<<(unsigned)nleaves, 512, 0, (cudaStream_t)stream>>>(uv, leaves, gamma, pfloor, smax);
+    return sg_check_launch("sg_max_wavespeed");
+}
+
+int sg_max_reduce(const double* vals, int64_t n, double* out, void* stream) {
+    max_reduce_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(vals, n, out);
+    return sg_check_launch("sg_max_reduce");
+}
+
+int sg_dt_from_smax(const double* s_pre, double cfl, double dx, double* dt, void* stream) {
+    dt_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(s_pre, cfl, dx, dt);
+    return sg_check_launch("sg_dt_from_smax");
+}
+
+}  // extern "C"

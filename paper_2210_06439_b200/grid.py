@@ -1,0 +1,234 @@
+"""Device-resident unigrid state and the batched full step.
+
+The reference advances a tree of 8^L SubGrids with one thread-pool task per
+leaf per kernel (reference driver.py:91-189): per step, mass = rho*dx^3, then
+6 x (ghost exchange + monopole + multipole), then dt from the pre-step max
+wave speed, then 3 x (ghost exchange + reconstruct + flux + update).  Here
+the same step runs on padded global fields resident in HBM:
+
+  U         (5, nz+4, n+4, n+4)     hydro state, pad 2 (= G ghosts)
+  mass      (nz+16, n+16, n+16)     pad 8 (the M2L 24^3 neighbourhood)
+  clusters  ((nz+16)/2, (n+16)/2, (n+16)/2, 4)   {M, Dx, Dy, Dz}
+  grav      (4, nz, n, n)           phi, gx, gy, gz
+  Q         (B, 5, 26, 10^3)        reconstruction (drop-in unfused path)
+
+with one launch per kernel over all B leaves, the ghost exchange replaced by
+an on-device periodic fill (plus the NCCL z-slab halo for P > 1, slab.py),
+and dt computed on device.  Results are bit-identical to the reference loop.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import batched as B
+from .batched import View
+from .kernels import GravityConfig, HydroConfig, KernelError, decode_flux_error, gravity_halo, gravity_params
+from .octree import HYDRO_FIELDS, morton_key
+from .slab import Slab, allreduce_max_, exchange_z_halo
+
+MASS_PAD = 8
+U_PAD = 2
+
+
+class UnigridState:
+    """One rank's z-slab of a periodic level-L unigrid, resident on a GPU."""
+
+    def __init__(self, level: int, hydro: HydroConfig | None = None, gravity: GravityConfig | None = None,
+                 slab: Slab | None = None, device=None, group=None):
+        B.require_device()
+        self.level = level
+        self.slab = slab or Slab(level)
+        if self.slab.level != level:
+            raise ValueError("slab level mismatch")
+        self.h = hydro or HydroConfig()
+        self.g = gravity or GravityConfig(expansion_order=1)
+        self.group = group
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        n, nz = self.slab.n, self.slab.nz
+        self.n, self.nz = n, nz
+        self.dx = 1.0 / n
+        self.halo = gravity_halo(self.g.theta)
+        self.rad2, self.eps2 = gravity_params(self.dx, self.g)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.uv = View(n, n, nz, U_PAD)
+        self.mv = View(n, n, nz, MASS_PAD)
+        self.gv = View(n, n, nz, 0)
+        self.U = torch.zeros((5,) + self.uv.padded_shape, **f64)
+        self.mass = torch.zeros(self.mv.padded_shape, **f64)
+        mz, my, mx = self.mv.padded_shape
+        self.clusters = torch.zeros((mz // 2, my // 2, mx // 2, 4), **f64)
+        self.grav = torch.zeros((4, nz, n, n), **f64)
+        self.leaves_host = self.slab.leaf_coords()
+        self.leaves = self.leaves_host.to(self.device)
+        self.nleaves = len(self.leaves_host)
+        nb = self.nleaves
+        self.Q = torch.empty((nb, 5, 26, 1000), **f64)
+        self.FX = torch.empty((nb, 5, 8, 8, 9), **f64)
+        self.FY = torch.empty((nb, 5, 8, 9, 8), **f64)
+        self.FZ = torch.empty((nb, 5, 9, 8, 8), **f64)
+        self.smax = torch.empty(nb, **f64)
+        self.ws = torch.empty(nb, **f64)
+        self.s_pre = torch.zeros(1, **f64)
+        self.dt = torch.zeros(1, **f64)
+        i32 = dict(dtype=torch.int32, device=self.device)
+        self.flux_err = torch.empty(nb, **i32)
+        self.upd_status = torch.empty(nb, **i32)
+        self.flux_latch = torch.full((nb,), -1, **i32)     # 0xFFFFFFFF
+        self.upd_latch = torch.full((nb,), -1, **i32)
+        self.timers = None  # optional {kernel: [(start, end) events]} for per-kernel timing
+
+    # -- host <-> device ---------------------------------------------------
+
+    def load(self, state: dict, *, global_arrays: bool = True) -> None:
+        """Upload rho, sx, sy, sz, E (global (n,n,n) arrays, or this slab's
+        (nz,n,n) part when global_arrays is False)."""
+        z0, nz, p = self.slab.z0, self.nz, U_PAD
+        for v, name in enumerate(HYDRO_FIELDS):
+            a = np.asarray(state[name], dtype=np.float64)
+            if global_arrays:
+                a = a[z0:z0 + nz]
+            self.U[v, p:p + nz, p:p + self.n, p:p + self.n].copy_(torch.from_numpy(np.ascontiguousarray(a)))
+        self.reset_errors()
+
+    def fetch(self) -> dict:
+        p = U_PAD
+        U = self.U[:, p:p + self.nz, p:p + self.n, p:p + self.n].cpu().numpy()
+        out = {name: U[v] for v, name in enumerate(HYDRO_FIELDS)}
+        g = self.grav.cpu().numpy()
+        for i, name in enumerate(("phi", "gx", "gy", "gz")):
+            out[name] = g[i]
+        return out
+
+    def reset_errors(self) -> None:
+        self.flux_latch.fill_(-1)
+        self.upd_latch.fill_(-1)
+
+    # -- per-kernel timing hooks -------------------------------------------
+
+    def _t(self, name: str):
+        if self.timers is None:
+            return None
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
+        self.timers.setdefault(name, []).append(ev)
+        return ev[1]
+
+    @staticmethod
+    def _done(ev) -> None:
+        if ev is not None:
+            ev.record()
+
+    # -- ghost / halo ------------------------------------------------------
+
+    def _halo(self, field: torch.Tensor, ncomp: int, view: View) -> None:
+        if self.slab.world == 1:
+            B.fill_periodic(field, ncomp, view, 7)
+        else:
+            B.fill_periodic(field, ncomp, view, 3)
+            exchange_z_halo(field.view((ncomp,) + view.padded_shape), view.pad, self.slab, self.group)
+
+    # -- the step pieces ---------------------------------------------------
+
+    def set_mass(self) -> None:
+        """driver.py:165-166: mass = rho * dx**3 (Python float pow, as the reference)."""
+        B.scale_copy(self.mass, MASS_PAD, self.U, U_PAD, self.n, self.n, self.nz, self.dx ** 3)
+
+    def gravity_iteration(self) -> None:
+        """driver.py:168-169: ghost exchange, then monopole and multipole for
+        every leaf; the multipole result overwrites the monopole one in the
+        shared phi/g outputs exactly as in the reference."""
+        self._halo(self.mass, 1, self.mv)
+        ev = self._t("cluster_aggregate")
+        B.cluster_aggregate(self.mass, self.dx, self.clusters)
+        self._done(ev)
+        ev = self._t("p2p")
+        B.p2p(self.mass, self.mv, self.leaves, self.nleaves, self.dx, self.rad2, self.eps2, self.halo,
+              self.grav, self.gv)
+        self._done(ev)
+        ev = self._t("m2l")
+        B.m2l(self.mass, self.mv, self.clusters, 0, self.leaves, self.nleaves, self.dx, self.rad2, self.eps2,
+              self.g.expansion_order, self.grav, self.gv)
+        self._done(ev)
+
+    def wavespeed_dt(self) -> None:
+        """driver.py:170-171 on device (+ MAX all-reduce across slabs)."""
+        ev = self._t("max_wavespeed")
+        B.max_wavespeed(self.U, self.uv, self.leaves, self.nleaves, self.h.gamma, self.h.positivity_floor,
+                        self.ws)
+        B.max_reduce(self.ws, self.nleaves, self.s_pre)
+        self._done(ev)
+        allreduce_max_(self.s_pre, self.slab, self.group)
+        B.dt_from_smax(self.s_pre, self.h.cfl, self.dx, self.dt)
+
+    def hydro_iteration(self) -> None:
+        """driver.py:173-174 / hydro_job 141-160 for every leaf."""
+        self._halo(self.U, 5, self.uv)
+        ev = self._t("reconstruct")
+        B.reconstruct(self.U, self.uv, self.leaves, self.nleaves, self.h.positivity_floor, self.Q)
+        self._done(ev)
+        ev = self._t("flux")
+        B.flux(self.Q, self.nleaves, self.h.gamma, self.FX, self.FY, self.FZ, self.smax, self.flux_err,
+               self.flux_latch)
+        self._done(ev)
+        ev = self._t("hydro_update")
+        B.hydro_update(self.U, self.uv, self.leaves, self.nleaves, self.FX, self.FY, self.FZ, self.smax,
+                       self.dt, 0.0, self.dx, self.h.cfl, self.upd_status, self.upd_latch)
+        self._done(ev)
+
+    def step(self, gravity_per_step: int = 6, hydro_per_step: int = 3) -> None:
+        """One reference timestep (driver.py:163-174)."""
+        if gravity_per_step:
+            self.set_mass()
+            for _ in range(gravity_per_step):
+                self.gravity_iteration()
+        self.wavespeed_dt()
+        for _ in range(hydro_per_step):
+            self.hydro_iteration()
+
+    # -- errors --------------------------------------------------------------
+
+    def check_errors(self, step: int | None = None) -> None:
+        """Raise the reference's KernelError for the first failing leaf in
+        Morton (leaf_iter) order, like driver._join (driver.py:83-88)."""
+        fl = self.flux_latch.cpu().numpy().view(np.uint32)
+        up = self.upd_latch.cpu().numpy().view(np.uint32)
+        bad = np.nonzero((fl != B.U32_OK) | (up != B.U32_OK))[0]
+        if not len(bad):
+            return
+        coords = self.slab.global_leaf_coords().numpy()
+        b = min(bad, key=lambda i: morton_key(*coords[i], self.level))
+        coord = tuple(int(c) for c in coords[b])
+        prefix = f"step {step}: " if step is not None else ""
+        if fl[b] != B.U32_OK:
+            code, cell = decode_flux_error(int(fl[b]))
+            what = "density" if code == 1 else "pressure"
+            raise KernelError(f"{prefix}non-positive {what} at a quadrature point of cell "
+                              f"(x={cell % 10 + 1}, y={(cell // 10) % 10 + 1}, z={cell // 100 + 1}) "
+                              f"[extended indices] of leaf {coord}")
+        kind, detail = int(up[b]) >> 16, int(up[b]) & 0xFFFF
+        if kind == 0:
+            raise KernelError(f"{prefix}dt must be positive, got {self.dt.item()}")
+        if kind == 1:
+            raise KernelError(f"{prefix}CFL violation at leaf {coord}: dt={self.dt.item():g}")
+        name = "rho" if kind == 2 else "E"
+        raise KernelError(f"{prefix}non-positive (or NaN) {name} after update at interior cell "
+                          f"(x={detail % 8}, y={(detail // 8) % 8}, z={detail // 64}) of leaf {coord}")
+
+
+def run_steps(state: dict, level: int, steps: int, *, hydro: HydroConfig | None = None,
+              gravity: GravityConfig | None = None, gravity_per_step: int = 6, slab: Slab | None = None,
+              group=None, check_every_step: bool = True) -> tuple[dict, list]:
+    """Public end-to-end entry: host arrays in, ``steps`` reference timesteps on
+    the device, host arrays out (plus the per-step dt values)."""
+    st = UnigridState(level, hydro, gravity, slab=slab, group=group)
+    st.load(state)
+    dts = []
+    for s in range(steps):
+        st.step(gravity_per_step)
+        dts.append(st.dt.item() if check_every_step else None)
+        if check_every_step:
+            st.check_errors(s)
+    st.check_errors()
+    return st.fetch(), dts
