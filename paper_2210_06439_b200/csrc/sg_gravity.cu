@@ -168,8 +168,13 @@ constexpr int NC = 12;          // clusters per axis
 constexpr int TAB_N = 15;       // |k| - 1/2 in 0..14 per axis
 constexpr int TAB_PITCH = 56;   // [inv x16 | inv3 x16 | inv5 x16 | pad 8]: 112 words == 16 mod 32
 constexpr int NEAR_R = 4;       // near-cell table covers |s| in 0..3
+// SMALL_NEAR variant: every near cluster has |k| <= 5/2 per axis (true iff
+// rad2 < 12.75 dx^2, e.g. theta = 0.34), so its cells lie in cube cells
+// [NB0, NB0+NBW) per axis -- staged in shared memory -- and |s| <= 3.
+constexpr int NB0 = 5, NBW = 14;
 constexpr size_t M2L_SMEM = sizeof(double) * TAB_N * TAB_N * TAB_PITCH +
-                            sizeof(double2) * NEAR_R * NEAR_R * NEAR_R + sizeof(double4) * NC * NC * NC;
+                            sizeof(double2) * NEAR_R * NEAR_R * NEAR_R + sizeof(double4) * NC * NC * NC +
+                            sizeof(double) * NBW * NBW * NBW;
 
 struct ClusterView {
     const double4* base;
@@ -223,7 +228,63 @@ __device__ __noinline__ void m2l_near(const double* __restrict__ mc, int64_t msy
     res[3] = gz_n;
 }
 
+// far-field term of one cluster, compiled.py:399-418 (same expression tree)
+// near-field sum of cluster (cz,cy,cx) in the SMALL_NEAR regime: masses from
+// the staged cube, 1/r~ and r~^-3 from the |s| table (same expression tree
+// as compiled.py:429-438 evaluated once per |s|), s*dx == the reference's
+// (t - ((b + o) + 1/2)) * dx exactly.  Masked terms are added as 0.0.
+__device__ __forceinline__ void m2l_near_small(const double* __restrict__ nm, const double2* __restrict__ near_tab,
+                                               int x, int y, int z, int cx, int cy, int cz, double dx,
+                                               double& acc_p, double& acc_x, double& acc_y, double& acc_z) {
+    double p_n = 0.0, gx_n = 0.0, gy_n = 0.0, gz_n = 0.0;
+    const int bxc = 2 * cx - 8, byc = 2 * cy - 8, bzc = 2 * cz - 8;
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+        const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+        const int si = x - (bxc + ox), sj = y - (byc + oy), sk = z - (bzc + oz);
+        const double m = nm[((bzc + oz + 8 - NB0) * NBW + (byc + oy + 8 - NB0)) * NBW + (bxc + ox + 8 - NB0)];
+        const double2 t = near_tab[(abs(sk) * NEAR_R + abs(sj)) * NEAR_R + abs(si)];
+        const bool ok = !signbit_d(t.x);
+        const double sx = mul((double)si, dx), sy = mul((double)sj, dx), sz = mul((double)sk, dx);
+        const double coms = mul(m, t.y);
+        p_n = add(p_n, ok ? -mul(m, t.x) : 0.0);
+        gx_n = add(gx_n, ok ? -mul(coms, sx) : 0.0);
+        gy_n = add(gy_n, ok ? -mul(coms, sy) : 0.0);
+        gz_n = add(gz_n, ok ? -mul(coms, sz) : 0.0);
+    }
+    acc_p = add(acc_p, p_n);
+    acc_x = add(acc_x, gx_n);
+    acc_y = add(acc_y, gy_n);
+    acc_z = add(acc_z, gz_n);
+}
+
 template <int ORDER>
+__device__ __forceinline__ void m2l_far(const double* __restrict__ row, int ax, const double4& c, double rx,
+                                        double ry, double rz, double& acc_p, double& acc_x, double& acc_y,
+                                        double& acc_z) {
+    const double inv = row[ax];
+    const double inv3 = row[16 + ax];
+    double p_f = -mul(c.x, inv);
+    const double gcom = mul(c.x, inv3);
+    double gx_f = -mul(gcom, rx);
+    double gy_f = -mul(gcom, ry);
+    double gz_f = -mul(gcom, rz);
+    if (ORDER == 1) {
+        const double inv5 = row[32 + ax];
+        const double dr = add(add(mul(c.y, rx), mul(c.z, ry)), mul(c.w, rz));
+        p_f = sub(p_f, mul(dr, inv3));
+        const double t3 = mul(mul(3.0, dr), inv5);
+        gx_f = sub(add(gx_f, mul(c.y, inv3)), mul(t3, rx));
+        gy_f = sub(add(gy_f, mul(c.z, inv3)), mul(t3, ry));
+        gz_f = sub(add(gz_f, mul(c.w, inv3)), mul(t3, rz));
+    }
+    acc_p = add(acc_p, p_f);
+    acc_x = add(acc_x, gx_f);
+    acc_y = add(acc_y, gy_f);
+    acc_z = add(acc_z, gz_f);
+}
+
+template <int ORDER, bool SMALL_NEAR>
 __global__ void __launch_bounds__(M2L_THREADS, 1)
 m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int64_t B, double dx,
            double rad2, double eps2, int i0, int i1, FieldView ov) {
@@ -231,6 +292,7 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
     double* tab = reinterpret_cast<double*>(smem_raw);
     double2* near_tab = reinterpret_cast<double2*>(tab + TAB_N * TAB_N * TAB_PITCH);
     double4* cl = reinterpret_cast<double4*>(near_tab + NEAR_R * NEAR_R * NEAR_R);
+    double* nm = reinterpret_cast<double*>(cl + NC * NC * NC);
     const int tid = threadIdx.x;
 
     // -- far geometry table, keyed by (|kx|,|ky|,|kz|) - 1/2 (compiled.py:394-414)
@@ -297,9 +359,14 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
                 cl[i] = make_double4(a.x, a.y, c2.x, c2.y);
             }
         }
-        __syncthreads();
-        if (!active) continue;
         const double* mc = leaf_origin(mv, leaves, b, 8);
+        if (SMALL_NEAR) {  // stage the near-field masses
+            for (int i = tid; i < NBW * NBW * NBW; i += M2L_THREADS) {
+                const int cx = i % NBW, cy = (i / NBW) % NBW, cz = i / (NBW * NBW);
+                nm[i] = __ldg(mc + (int64_t)(cz + NB0) * mv.sz + (int64_t)(cy + NB0) * mv.sy + (cx + NB0));
+            }
+        }
+        __syncthreads();
         double acc_p = 0.0, acc_x = 0.0, acc_y = 0.0, acc_z = 0.0;
 #pragma unroll 1
         for (int cz = 0; cz < NC; ++cz) {
@@ -311,48 +378,51 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
                 const int ay = fold(y - 2 * cy + 7);
                 const double* row = tab + (az * TAB_N + ay) * TAB_PITCH;
                 const double4* crow = cl + (cz * NC + cy) * NC;
+                // r^2 grows with |kx|, so a row holds a near cluster iff its
+                // |kx| = 1/2 entry is near.  Warp-uniform choice: rows with no
+                // near cluster for any lane run branch-free.
+                if (!__any_sync(0xffffffffu, signbit_d(row[0]))) {
 #pragma unroll
-                for (int cx = 0; cx < NC; ++cx) {
-                    const double inv = row[axv[cx]];
-                    const double rx = rxv[cx];
-                    if (!signbit_d(inv)) {
-                        // far: compiled.py:399-418
-                        const double inv3 = row[16 + axv[cx]];
-                        const double4 c = crow[cx];
-                        double p_f = -mul(c.x, inv);
-                        const double gcom = mul(c.x, inv3);
-                        double gx_f = -mul(gcom, rx);
-                        double gy_f = -mul(gcom, ry);
-                        double gz_f = -mul(gcom, rz);
-                        if (ORDER == 1) {
-                            const double inv5 = row[32 + axv[cx]];
-                            const double dr = add(add(mul(c.y, rx), mul(c.z, ry)), mul(c.w, rz));
-                            p_f = sub(p_f, mul(dr, inv3));
-                            const double t3 = mul(mul(3.0, dr), inv5);
-                            gx_f = sub(add(gx_f, mul(c.y, inv3)), mul(t3, rx));
-                            gy_f = sub(add(gy_f, mul(c.z, inv3)), mul(t3, ry));
-                            gz_f = sub(add(gz_f, mul(c.w, inv3)), mul(t3, rz));
+                    for (int cx = 0; cx < NC; ++cx)
+                        m2l_far<ORDER>(row, axv[cx], crow[cx], rxv[cx], ry, rz, acc_p, acc_x, acc_y, acc_z);
+                } else if (SMALL_NEAR) {
+                    // rows holding near clusters: compact loop, per-lane branch
+#pragma unroll 1
+                    for (int cx = 0; cx < NC; ++cx) {
+                        const int ax = fold(x - 2 * cx + 7);
+                        if (!signbit_d(row[ax])) {
+                            const double rx = mul(sub(tx, add((double)(2 * cx - 8), 1.0)), dx);
+                            m2l_far<ORDER>(row, ax, crow[cx], rx, ry, rz, acc_p, acc_x, acc_y, acc_z);
+                        } else {
+                            m2l_near_small(nm, near_tab, x, y, z, cx, cy, cz, dx, acc_p, acc_x, acc_y, acc_z);
                         }
-                        acc_p = add(acc_p, p_f);
-                        acc_x = add(acc_x, gx_f);
-                        acc_y = add(acc_y, gy_f);
-                        acc_z = add(acc_z, gz_f);
-                    } else {
-                        double r[4];
-                        m2l_near(mc, mv.sy, mv.sz, near_tab, x, y, z, cx, cy, cz, dx, eps2, r);
-                        acc_p = add(acc_p, r[0]);
-                        acc_x = add(acc_x, r[1]);
-                        acc_y = add(acc_y, r[2]);
-                        acc_z = add(acc_z, r[3]);
+                    }
+                } else {
+#pragma unroll 1
+                    for (int cx = 0; cx < NC; ++cx) {
+                        const int ax = fold(x - 2 * cx + 7);
+                        if (!signbit_d(row[ax])) {
+                            const double rx = mul(sub(tx, add((double)(2 * cx - 8), 1.0)), dx);
+                            m2l_far<ORDER>(row, ax, crow[cx], rx, ry, rz, acc_p, acc_x, acc_y, acc_z);
+                        } else {
+                            double r[4];
+                            m2l_near(mc, mv.sy, mv.sz, near_tab, x, y, z, cx, cy, cz, dx, eps2, r);
+                            acc_p = add(acc_p, r[0]);
+                            acc_x = add(acc_x, r[1]);
+                            acc_y = add(acc_y, r[2]);
+                            acc_z = add(acc_z, r[3]);
+                        }
                     }
                 }
             }
         }
-        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy + x;
-        o[0] = acc_p;
-        o[ov.comp_stride] = acc_x;
-        o[2 * ov.comp_stride] = acc_y;
-        o[3 * ov.comp_stride] = acc_z;
+        if (active) {  // inactive lanes still computed: the row vote needs full warps
+            double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy + x;
+            o[0] = acc_p;
+            o[ov.comp_stride] = acc_x;
+            o[2 * ov.comp_stride] = acc_y;
+            o[3 * ov.comp_stride] = acc_z;
+        }
     }
 }
 
@@ -432,14 +502,19 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     cv.off = (pad - 8) / 2;
     FieldView ov = make_view(out, onx, ony, onz, 0, out_leaf_stride);
     const int64_t grid = nleaves < sm_count() ? nleaves : sm_count();
+    // every near cluster within |k| <= 5/2 per axis (conservative margin)
+    const bool small_near = rad2 < 12.5 * dx * dx;
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M2L_SMEM);
+        kern<<<(unsigned)grid, M2L_THREADS, M2L_SMEM, (cudaStream_t)stream>>>(mv, cv, leaves, nleaves, dx, rad2,
+                                                                             eps2, i0, i1, ov);
+    };
     if (order == 1) {
-        cudaFuncSetAttribute(m2l_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M2L_SMEM);
-        m2l_kernel<1><<<(unsigned)grid, M2L_THREADS, M2L_SMEM, (cudaStream_t)stream>>>(
-            mv, cv, leaves, nleaves, dx, rad2, eps2, i0, i1, ov);
+        if (small_near) launch(m2l_kernel<1, true>);
+        else launch(m2l_kernel<1, false>);
     } else {
-        cudaFuncSetAttribute(m2l_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M2L_SMEM);
-        m2l_kernel<0><<<(unsigned)grid, M2L_THREADS, M2L_SMEM, (cudaStream_t)stream>>>(
-            mv, cv, leaves, nleaves, dx, rad2, eps2, i0, i1, ov);
+        if (small_near) launch(m2l_kernel<0, true>);
+        else launch(m2l_kernel<0, false>);
     }
     return sg_check_launch("sg_m2l");
 }
