@@ -70,11 +70,15 @@ int sg_p2p(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
  * mass view with even pad >= 8 (near-field cells), clusters from
  * sg_cluster_aggregate over the same padded array (cluster_leaf_stride in
  * doubles for stacked blocks, else 0), order in {0,1}, flat interior target
- * range [i0, i1) (the reference's run(i0, i1) chunk), out view as sg_p2p. */
+ * range [i0, i1) (the reference's run(i0, i1) chunk), out view as sg_p2p.
+ * workspace: device scratch of >= sg_m2l_workspace_bytes(nleaves) bytes
+ * (near-field partial sums; contents are not an output). */
+int64_t sg_m2l_workspace_bytes(int64_t nleaves);
 int sg_m2l(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
            const double *clusters, int64_t cluster_leaf_stride, const int32_t *leaves, int64_t nleaves,
            double dx, double rad2, double eps2, int32_t order, int32_t i0, int32_t i1, double *out,
-           int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, void *stream);
+           int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, double *workspace,
+           int64_t workspace_bytes, void *stream);
 
 /* ------------------------------------------------------------------ hydro */
 

@@ -25,7 +25,8 @@ SIGNATURES = {
     "sg_p2p": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _d, _d, _i32,
                _p, _i64, _i64, _i64, _i64, _p],
     "sg_m2l": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _p, _i64, _d, _d, _d, _i32, _i32, _i32,
-               _p, _i64, _i64, _i64, _i64, _p],
+               _p, _i64, _i64, _i64, _i64, _p, _i64, _p],
+    "sg_m2l_workspace_bytes": [_i64],
     "sg_reconstruct": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _p, _p],
     "sg_flux": [_p, _i64, _d, _p, _p, _p, _p, _p, _p, _p],
     "sg_hydro_update": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _p, _p, _p, _p, _p, _d, _d, _d,
@@ -37,6 +38,9 @@ SIGNATURES = {
     "sg_scale_copy": [_p, _i32, _p, _i32, _i64, _i64, _i64, _d, _p],
     "sg_fp64_peak": [ctypes.c_int, ctypes.c_int, _p, ctypes.POINTER(_i64), _p],
 }
+
+
+RESTYPES = {"sg_m2l_workspace_bytes": _i64}
 
 
 class SGUnavailable(RuntimeError):
@@ -62,7 +66,7 @@ def load(path: Path | None = None):
     for name, argtypes in SIGNATURES.items():
         fn = getattr(L, name)
         fn.argtypes = argtypes
-        fn.restype = ctypes.c_int
+        fn.restype = RESTYPES.get(name, ctypes.c_int)
     L.sg_last_error.argtypes = []
     L.sg_last_error.restype = ctypes.c_char_p
     if L.sg_abi_version() != ABI_VERSION:

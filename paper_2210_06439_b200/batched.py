@@ -77,11 +77,27 @@ def p2p(mass, mv: View, leaves, nleaves: int, dx: float, rad2: float, eps2: floa
               ov.leaf_stride, _stream())
 
 
+_WORKSPACE: dict = {}
+
+
+def m2l_workspace(nleaves: int, device=None) -> torch.Tensor:
+    """Cached per-device scratch for sg_m2l (grows on demand)."""
+    need = int(_lib.load().sg_m2l_workspace_bytes(nleaves))
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    ws = _WORKSPACE.get(dev)
+    if ws is None or ws.numel() * 8 < need:
+        ws = torch.empty((need + 7) // 8, dtype=torch.float64, device=dev)
+        _WORKSPACE[dev] = ws
+    return ws
+
+
 def m2l(mass, mv: View, clusters, cluster_leaf_stride: int, leaves, nleaves: int, dx: float, rad2: float,
-        eps2: float, order: int, out, ov: View, i0: int = 0, i1: int = 512) -> None:
+        eps2: float, order: int, out, ov: View, i0: int = 0, i1: int = 512, workspace=None) -> None:
+    ws = workspace if workspace is not None else m2l_workspace(nleaves, mass.device)
     _lib.call("sg_m2l", _f64(mass), mv.nx, mv.ny, mv.nz, mv.pad, mv.leaf_stride, _f64(clusters),
               cluster_leaf_stride, _ptr(leaves), nleaves, float(dx), float(rad2), float(eps2), int(order),
-              int(i0), int(i1), _f64(out), ov.nx, ov.ny, ov.nz, ov.leaf_stride, _stream())
+              int(i0), int(i1), _f64(out), ov.nx, ov.ny, ov.nz, ov.leaf_stride, _f64(ws), ws.numel() * 8,
+              _stream())
 
 
 def reconstruct(U, uv: View, leaves, nleaves: int, floor: float, Q) -> None:

@@ -174,7 +174,8 @@ constexpr int NEAR_R = 4;       // near-cell table covers |s| in 0..3
 constexpr int NB0 = 5, NBW = 14;
 constexpr size_t M2L_SMEM = sizeof(double) * TAB_N * TAB_N * TAB_PITCH +
                             sizeof(double2) * NEAR_R * NEAR_R * NEAR_R + sizeof(double4) * NC * NC * NC +
-                            sizeof(double) * NBW * NBW * NBW;
+                            sizeof(double) * NBW * NBW * NBW + sizeof(int) * 32;
+constexpr int64_t M2L_WORK_PER_CTA = 27 * 4 * M2L_THREADS;  // doubles
 
 struct ClusterView {
     const double4* base;
@@ -235,8 +236,11 @@ __device__ __noinline__ void m2l_near(const double* __restrict__ mc, int64_t msy
 // (t - ((b + o) + 1/2)) * dx exactly.  Masked terms are added as 0.0.
 __device__ __forceinline__ void m2l_near_small(const double* __restrict__ nm, const double2* __restrict__ near_tab,
                                                int x, int y, int z, int cx, int cy, int cz, double dx,
-                                               double& acc_p, double& acc_x, double& acc_y, double& acc_z) {
-    double p_n = 0.0, gx_n = 0.0, gy_n = 0.0, gz_n = 0.0;
+                                               double& p_n, double& gx_n, double& gy_n, double& gz_n) {
+    p_n = 0.0;
+    gx_n = 0.0;
+    gy_n = 0.0;
+    gz_n = 0.0;
     const int bxc = 2 * cx - 8, byc = 2 * cy - 8, bzc = 2 * cz - 8;
 #pragma unroll
     for (int o = 0; o < 8; ++o) {
@@ -252,10 +256,13 @@ __device__ __forceinline__ void m2l_near_small(const double* __restrict__ nm, co
         gy_n = add(gy_n, ok ? -mul(coms, sy) : 0.0);
         gz_n = add(gz_n, ok ? -mul(coms, sz) : 0.0);
     }
-    acc_p = add(acc_p, p_n);
-    acc_x = add(acc_x, gx_n);
-    acc_y = add(acc_y, gy_n);
-    acc_z = add(acc_z, gz_n);
+}
+
+// cluster index along one axis whose |k| - 1/2 equals a (k = t + 15/2 - 2c):
+// exactly one of (t+7-a)/2, (t+8+a)/2 is an integer
+__device__ __forceinline__ int cluster_of(int t, int a) {
+    const int u = t + 7 - a;
+    return (u & 1) ? (t + 8 + a) >> 1 : u >> 1;
 }
 
 template <int ORDER>
@@ -287,13 +294,16 @@ __device__ __forceinline__ void m2l_far(const double* __restrict__ row, int ax, 
 template <int ORDER, bool SMALL_NEAR>
 __global__ void __launch_bounds__(M2L_THREADS, 1)
 m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int64_t B, double dx,
-           double rad2, double eps2, int i0, int i1, FieldView ov) {
+           double rad2, double eps2, int i0, int i1, FieldView ov, double* __restrict__ work) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* tab = reinterpret_cast<double*>(smem_raw);
     double2* near_tab = reinterpret_cast<double2*>(tab + TAB_N * TAB_N * TAB_PITCH);
     double4* cl = reinterpret_cast<double4*>(near_tab + NEAR_R * NEAR_R * NEAR_R);
     double* nm = reinterpret_cast<double*>(cl + NC * NC * NC);
+    int* near_slot = reinterpret_cast<int*>(nm + NBW * NBW * NBW);  // 27 entries
     const int tid = threadIdx.x;
+    // CTA-private near-sum workspace: [slot < 27][comp 4][thread 512]
+    double* wk = work + (int64_t)blockIdx.x * (27 * 4 * M2L_THREADS) + tid;
 
     // -- far geometry table, keyed by (|kx|,|ky|,|kz|) - 1/2 (compiled.py:394-414)
     for (int e = tid; e < TAB_N * TAB_N * TAB_N; e += M2L_THREADS) {
@@ -326,6 +336,16 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
             near_tab[tid] = make_double2(invs, mul(mul(invs, invs), invs));
         } else {
             near_tab[tid] = make_double2(-1.0, 0.0);
+        }
+    }
+
+    __syncthreads();
+    if (SMALL_NEAR && tid == 0) {
+        // (|kx|,|ky|,|kz|) - 1/2 in {0,1,2}^3 -> compact slot of the near ones
+        int k = 0;
+        for (int e = 0; e < 27; ++e) {
+            const int ax = e % 3, ay = (e / 3) % 3, az = e / 9;
+            near_slot[e] = signbit_d(tab[(az * TAB_N + ay) * TAB_PITCH + ax]) ? k++ : -1;
         }
     }
 
@@ -367,6 +387,23 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
             }
         }
         __syncthreads();
+        if (SMALL_NEAR) {
+            // every target has its near clusters at the same (|kx|,|ky|,|kz|)
+            // combos, so all lanes evaluate them together (no divergence)
+#pragma unroll 1
+            for (int e = 0; e < 27; ++e) {
+                const int k = near_slot[e];
+                if (k < 0) continue;
+                const int ax = e % 3, ay = (e / 3) % 3, az = e / 9;
+                double p, gx, gy, gz;
+                m2l_near_small(nm, near_tab, x, y, z, cluster_of(x, ax), cluster_of(y, ay), cluster_of(z, az), dx,
+                               p, gx, gy, gz);
+                wk[(k * 4 + 0) * M2L_THREADS] = p;
+                wk[(k * 4 + 1) * M2L_THREADS] = gx;
+                wk[(k * 4 + 2) * M2L_THREADS] = gy;
+                wk[(k * 4 + 3) * M2L_THREADS] = gz;
+            }
+        }
         double acc_p = 0.0, acc_x = 0.0, acc_y = 0.0, acc_z = 0.0;
 #pragma unroll 1
         for (int cz = 0; cz < NC; ++cz) {
@@ -386,16 +423,24 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
                     for (int cx = 0; cx < NC; ++cx)
                         m2l_far<ORDER>(row, axv[cx], crow[cx], rxv[cx], ry, rz, acc_p, acc_x, acc_y, acc_z);
                 } else if (SMALL_NEAR) {
-                    // rows holding near clusters: compact loop, per-lane branch
-#pragma unroll 1
+                    // rows holding near clusters: far term for every cluster,
+                    // near lanes take their prologue sum instead (same order)
+                    const int rowslot = (az * 3 + ay) * 3;
+#pragma unroll
                     for (int cx = 0; cx < NC; ++cx) {
-                        const int ax = fold(x - 2 * cx + 7);
-                        if (!signbit_d(row[ax])) {
-                            const double rx = mul(sub(tx, add((double)(2 * cx - 8), 1.0)), dx);
-                            m2l_far<ORDER>(row, ax, crow[cx], rx, ry, rz, acc_p, acc_x, acc_y, acc_z);
-                        } else {
-                            m2l_near_small(nm, near_tab, x, y, z, cx, cy, cz, dx, acc_p, acc_x, acc_y, acc_z);
+                        double p = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+                        m2l_far<ORDER>(row, axv[cx], crow[cx], rxv[cx], ry, rz, p, gx, gy, gz);
+                        if (signbit_d(row[axv[cx]])) {
+                            const int k = near_slot[rowslot + axv[cx]];
+                            p = wk[(k * 4 + 0) * M2L_THREADS];
+                            gx = wk[(k * 4 + 1) * M2L_THREADS];
+                            gy = wk[(k * 4 + 2) * M2L_THREADS];
+                            gz = wk[(k * 4 + 3) * M2L_THREADS];
                         }
+                        acc_p = add(acc_p, p);
+                        acc_x = add(acc_x, gx);
+                        acc_y = add(acc_y, gy);
+                        acc_z = add(acc_z, gz);
                     }
                 } else {
 #pragma unroll 1
@@ -480,10 +525,16 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     return sg_check_launch("sg_p2p");
 }
 
+int64_t sg_m2l_workspace_bytes(int64_t nleaves) {
+    const int64_t grid = nleaves < sm_count() ? nleaves : sm_count();
+    return (grid > 0 ? grid : 1) * M2L_WORK_PER_CTA * (int64_t)sizeof(double);
+}
+
 int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
            const double* clusters, int64_t cluster_leaf_stride, const int32_t* leaves, int64_t nleaves,
            double dx, double rad2, double eps2, int32_t order, int32_t i0, int32_t i1, double* out,
-           int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, void* stream) {
+           int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, double* workspace,
+           int64_t workspace_bytes, void* stream) {
     if (pad < 8 || (pad & 1)) {
         sg_set_error("sg_m2l: mass pad must be even and >= 8 (got %d)", pad);
         return SG_EINVAL;
@@ -493,6 +544,11 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
         return SG_EINVAL;
     }
     if (nleaves <= 0 || i1 <= i0) return SG_OK;
+    if (!workspace || workspace_bytes < sg_m2l_workspace_bytes(nleaves)) {
+        sg_set_error("sg_m2l: workspace of %lld bytes required (got %lld)",
+                     (long long)sg_m2l_workspace_bytes(nleaves), (long long)workspace_bytes);
+        return SG_EINVAL;
+    }
     FieldView mv = make_view(mass, nx, ny, nz, pad, leaf_stride);
     ClusterView cv;
     cv.base = reinterpret_cast<const double4*>(clusters);
@@ -507,7 +563,7 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M2L_SMEM);
         kern<<<(unsigned)grid, M2L_THREADS, M2L_SMEM, (cudaStream_t)stream>>>(mv, cv, leaves, nleaves, dx, rad2,
-                                                                             eps2, i0, i1, ov);
+                                                                             eps2, i0, i1, ov, workspace);
     };
     if (order == 1) {
         if (small_near) launch(m2l_kernel<1, true>);
