@@ -26,7 +26,7 @@ from . import batched as B
 from .batched import View
 from .kernels import GravityConfig, HydroConfig, KernelError, decode_flux_error, gravity_halo, gravity_params
 from .octree import HYDRO_FIELDS, morton_key
-from .slab import Slab, allreduce_max_, exchange_z_halo
+from .slab import Slab, allreduce_max_, exchange_z_halo, exchange_z_halo_local
 
 MASS_PAD = 8
 U_PAD = 2
@@ -140,6 +140,9 @@ class UnigridState:
         every leaf; the multipole result overwrites the monopole one in the
         shared phi/g outputs exactly as in the reference."""
         self._halo(self.mass, 1, self.mv)
+        self.gravity_kernels()
+
+    def gravity_kernels(self) -> None:
         ev = self._t("cluster_aggregate")
         B.cluster_aggregate(self.mass, self.dx, self.clusters)
         self._done(ev)
@@ -154,17 +157,23 @@ class UnigridState:
 
     def wavespeed_dt(self) -> None:
         """driver.py:170-171 on device (+ MAX all-reduce across slabs)."""
+        self.wavespeed_local()
+        allreduce_max_(self.s_pre, self.slab, self.group)
+        B.dt_from_smax(self.s_pre, self.h.cfl, self.dx, self.dt)
+
+    def wavespeed_local(self) -> None:
         ev = self._t("max_wavespeed")
         B.max_wavespeed(self.U, self.uv, self.leaves, self.nleaves, self.h.gamma, self.h.positivity_floor,
                         self.ws)
         B.max_reduce(self.ws, self.nleaves, self.s_pre)
         self._done(ev)
-        allreduce_max_(self.s_pre, self.slab, self.group)
-        B.dt_from_smax(self.s_pre, self.h.cfl, self.dx, self.dt)
 
     def hydro_iteration(self) -> None:
         """driver.py:173-174 / hydro_job 141-160 for every leaf."""
         self._halo(self.U, 5, self.uv)
+        self.hydro_kernels()
+
+    def hydro_kernels(self) -> None:
         ev = self._t("reconstruct")
         B.reconstruct(self.U, self.uv, self.leaves, self.nleaves, self.h.positivity_floor, self.Q)
         self._done(ev)
@@ -215,6 +224,57 @@ class UnigridState:
         name = "rho" if kind == 2 else "E"
         raise KernelError(f"{prefix}non-positive (or NaN) {name} after update at interior cell "
                           f"(x={detail % 8}, y={(detail // 8) % 8}, z={detail // 64}) of leaf {coord}")
+
+
+class LocalSlabs:
+    """The z-slab decomposition with all P slabs in one process on one
+    device: same kernels, same halo planes as the NCCL path, exchanged by
+    device copies.  Used to check that results are bitwise P-invariant."""
+
+    def __init__(self, level: int, world: int, hydro: HydroConfig | None = None,
+                 gravity: GravityConfig | None = None):
+        self.states = [UnigridState(level, hydro, gravity, slab=Slab(level, r, world)) for r in range(world)]
+        self.world = world
+
+    def load(self, state: dict) -> None:
+        for s in self.states:
+            s.load(state)
+
+    def _halo_all(self, name: str, ncomp: int, view: View) -> None:
+        fields = []
+        for s in self.states:
+            f = getattr(s, name)
+            B.fill_periodic(f, ncomp, view, 3)
+            fields.append(f.view((ncomp,) + view.padded_shape))
+        exchange_z_halo_local(fields, view.pad, self.states[0].nz)
+
+    def step(self, gravity_per_step: int = 6, hydro_per_step: int = 3) -> None:
+        st = self.states
+        if gravity_per_step:
+            for s in st:
+                s.set_mass()
+            for _ in range(gravity_per_step):
+                self._halo_all("mass", 1, st[0].mv)
+                for s in st:
+                    s.gravity_kernels()
+        for s in st:
+            s.wavespeed_local()
+        s_pre = torch.stack([s.s_pre for s in st]).max(dim=0).values
+        for s in st:
+            s.s_pre.copy_(s_pre)
+            B.dt_from_smax(s.s_pre, s.h.cfl, s.dx, s.dt)
+        for _ in range(hydro_per_step):
+            self._halo_all("U", 5, st[0].uv)
+            for s in st:
+                s.hydro_kernels()
+
+    def check_errors(self, step: int | None = None) -> None:
+        for s in self.states:
+            s.check_errors(step)
+
+    def fetch(self) -> dict:
+        parts = [s.fetch() for s in self.states]
+        return {k: np.concatenate([p[k] for p in parts], axis=0) for k in parts[0]}
 
 
 def run_steps(state: dict, level: int, steps: int, *, hydro: HydroConfig | None = None,

@@ -95,6 +95,19 @@ def exchange_z_halo(field: torch.Tensor, pad: int, slab: Slab, group=None) -> No
         req.wait()
 
 
+def exchange_z_halo_local(fields: list, pad: int, nz: int) -> None:
+    """The same exchange between P slabs held by one process (slab r at
+    fields[r], each (ncomp, nz+2p, Y, X)): used to run the z-slab
+    decomposition on a single device, e.g. to check P-invariance."""
+    P = len(fields)
+    if nz < pad:
+        raise ValueError(f"slab of {nz} planes is thinner than the halo ({pad})")
+    for r, f in enumerate(fields):
+        down, up = fields[(r - 1) % P], fields[(r + 1) % P]
+        f[:, 0:pad].copy_(down[:, nz:nz + pad])
+        f[:, nz + pad:nz + 2 * pad].copy_(up[:, pad:2 * pad])
+
+
 def allreduce_max_(t: torch.Tensor, slab: Slab, group=None) -> None:
     """dt reduction across ranks: MAX is order-independent, so dt is bitwise
     identical for every P (driver.py:170-171)."""

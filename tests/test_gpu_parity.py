@@ -281,3 +281,27 @@ def test_cfg5_level2_ten_steps(manifest):
 
 def test_cfg5_level4_ten_steps(manifest):
     _check_cfg5(manifest["cfg5_L4"], 4)
+
+
+# -- z-slab decomposition: bitwise P-invariance against the same goldens ----------
+
+@pytest.mark.parametrize("level,world", [(2, 2), (2, 4), (4, 8)])
+def test_cfg5_slabs_match_golden(manifest, level, world):
+    m = manifest[f"cfg5_L{level}"]
+    st = scenarios.config5_state(level)
+    U = np.stack([st[k] for k in octree.HYDRO_FIELDS])
+    if digest(U) != m["input_digest"]:
+        pytest.skip("config-5 generator differs on this host (libm)")
+    ls = G.LocalSlabs(level, world, K.HydroConfig(gamma=float.fromhex(m["gamma"])),
+                      K.GravityConfig(theta=0.34, eps=0.5, expansion_order=1))
+    ls.load(st)
+    for s in range(m["steps"]):
+        ls.step()
+        ls.check_errors(s)
+        assert ls.states[0].dt.item().hex() == m["dts"][s]
+        if str(s) in m["gravity_digests"]:
+            g = np.concatenate([u.grav.cpu().numpy() for u in ls.states], axis=1)
+            assert digest(g) == m["gravity_digests"][str(s)], s
+    out = ls.fetch()
+    for k in octree.HYDRO_FIELDS:
+        assert digest(out[k]) == m["final_field_digests"][k], k

@@ -1,0 +1,58 @@
+"""Multi-process z-slab plumbing on CPU: world_size 2 and 4 over gloo run the
+same torch.distributed halo exchange and MAX reduction the NCCL path uses,
+and must reproduce the periodic padding of the global field exactly."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2210_06439_b200.slab import Slab, allreduce_max_, exchange_z_halo
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, level, pad, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        slab = Slab(level, rank, world)
+        n = slab.n
+        g = np.random.default_rng(2).uniform(size=(3, n, n, n))
+        want = np.pad(g, ((0, 0), (pad, pad), (pad, pad), (pad, pad)), mode="wrap")
+        f = torch.zeros((3, slab.nz + 2 * pad, n + 2 * pad, n + 2 * pad), dtype=torch.float64)
+        f[:, pad:pad + slab.nz] = torch.from_numpy(want[:, pad + slab.z0:pad + slab.z0 + slab.nz])
+        exchange_z_halo(f, pad, slab)
+        ok = np.array_equal(f.numpy(), want[:, slab.z0:slab.z0 + slab.nz + 2 * pad])
+        t = torch.tensor([float(rank + 1) * 0.5], dtype=torch.float64)
+        allreduce_max_(t, slab)
+        q.put((rank, ok, t.item()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,level,pad", [(2, 2, 8), (2, 2, 2), (4, 2, 8)])
+def test_gloo_halo_exchange_matches_periodic_pad(world, level, pad):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, level, pad, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, mx in res:
+        assert ok, f"rank {rank} halo mismatch"
+        assert mx == world * 0.5
