@@ -98,6 +98,13 @@ int sg_reconstruct(const double *U, int64_t nx, int64_t ny, int64_t nz, int32_t 
 int sg_flux(const double *Q, int64_t nleaves, double gamma, double *FX, double *FY, double *FZ,
             double *smax, uint32_t *err, uint32_t *latch, void *stream);
 
+/* Fused reconstruct + flux for the batched step: same outputs, smax, err and
+ * latch as sg_reconstruct followed by sg_flux (bit-identical), without
+ * materialising Q.  U view as sg_reconstruct. */
+int sg_hydro_fused(const double *U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+                   const int32_t *leaves, int64_t nleaves, double floor_, double gamma, double *FX, double *FY,
+                   double *FZ, double *smax, uint32_t *err, uint32_t *latch, void *stream);
+
 /* Replaces compiled.hydro_update_kernel (compiled.py:265-278) plus the checks
  * of kernels.hydro_update (kernels/__init__.py:165-188), in place on the U
  * view.  dt from *dt_dev when non-NULL (device-computed, graph-capturable),

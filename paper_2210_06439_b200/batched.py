@@ -110,6 +110,14 @@ def flux(Q, nleaves: int, gamma: float, FX, FY, FZ, smax, err, latch=None) -> No
               _ptr(err), _ptr(latch), _stream())
 
 
+def hydro_fused(U, uv: View, leaves, nleaves: int, floor: float, gamma: float, FX, FY, FZ, smax, err,
+                latch=None) -> None:
+    """reconstruct + flux without materialising Q (bit-identical outputs)."""
+    _lib.call("sg_hydro_fused", _f64(U), uv.nx, uv.ny, uv.nz, uv.pad, uv.leaf_stride, _ptr(leaves), nleaves,
+              float(floor), float(gamma), _f64(FX), _f64(FY), _f64(FZ), _f64(smax), _ptr(err), _ptr(latch),
+              _stream())
+
+
 def hydro_update(U, uv: View, leaves, nleaves: int, FX, FY, FZ, smax, dt_dev, dt: float, dx: float,
                  cfl: float, status, latch=None) -> None:
     _lib.call("sg_hydro_update", _f64(U), uv.nx, uv.ny, uv.nz, uv.pad, uv.leaf_stride, _ptr(leaves),

@@ -253,6 +253,196 @@ flux_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX,
 }
 
 // ---------------------------------------------------------------------------
+// fused reconstruct + flux (batched step path): U block and per-cell
+// {uc, minmod slopes} in shared memory, every quadrature state rebuilt on the
+// fly with the reconstruct_kernel expression tree -- Q (1.04 MB/subgrid) is
+// never written.  Outputs/status identical to sg_reconstruct + sg_flux.
+// ---------------------------------------------------------------------------
+#ifndef FUSED_NT
+#define FUSED_NT 512
+#endif
+constexpr int FUSED_THREADS = FUSED_NT;  // faces t, t+NT, ... of the axis-major list of 1728
+constexpr int CELL_REC = 20;        // uc[5], slope[5][3]
+constexpr size_t FUSED_SMEM = sizeof(double) * (NVAR * 1728 + CELL_REC * REC_CELLS);
+
+// compiled.py:74-97 for one (cell, direction), cell record read from smem
+__device__ __forceinline__ void rebuild_state(const double* __restrict__ C, int cell, int d, double floor_,
+                                              double onepf, double& rho, double& sx, double& sy, double& sz,
+                                              double& en) {
+    const double fdz = c_dirs[d][0], fdy = c_dirs[d][1], fdx = c_dirs[d][2];
+    double r[NVAR];
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) {
+        const double* c = C + cell;
+        r[v] = add(c[v * REC_CELLS],
+                   mul(0.5, add(add(mul(fdx, c[(NVAR + v * 3 + 0) * REC_CELLS]), mul(fdy, c[(NVAR + v * 3 + 1) * REC_CELLS])),
+                                mul(fdz, c[(NVAR + v * 3 + 2) * REC_CELLS]))));
+    }
+    rho = r[0] < floor_ ? floor_ : r[0];
+    en = r[4] < floor_ ? floor_ : r[4];
+    sx = r[1];
+    sy = r[2];
+    sz = r[3];
+    const double ke = dvd(mul(0.5, add(add(mul(sx, sx), mul(sy, sy)), mul(sz, sz))), rho);
+    const double emin = add(mul(ke, onepf), floor_);
+    en = en < emin ? emin : en;
+}
+
+// one face (compiled.py:120-262); axis is warp-uniform at run time
+__device__ __forceinline__ void fused_face(const double* __restrict__ C, int axis, int fi, int64_t b,
+                                           double floor_, double onepf, double gamma, double gm1,
+                                           double* __restrict__ FX, double* __restrict__ FY,
+                                           double* __restrict__ FZ, double& smax, uint32_t& err) {
+    const int nj = axis == 0 ? NIN : NIN + 1;
+    const int nk = axis == 0 ? NIN + 1 : NIN;
+    const int k = fi % nk, j = (fi / nk) % nj, i = fi / (nk * nj);
+    int zl, zr, yl, yr, xl, xr;
+    if (axis == 0) {
+        zl = zr = i + 1; yl = yr = j + 1; xl = k; xr = k + 1;
+    } else if (axis == 1) {
+        zl = zr = i + 1; yl = j; yr = j + 1; xl = xr = k + 1;
+    } else {
+        zl = j; zr = j + 1; yl = yr = i + 1; xl = xr = k + 1;
+    }
+    const int cl_ = (zl * NRC + yl) * NRC + xl, cr_ = (zr * NRC + yr) * NRC + xr;
+    const uint32_t kbase = (uint32_t)((((axis * 8 + i) * 9 + j) * 9 + k) * 9);
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0, f4 = 0.0;
+#pragma unroll 1
+    for (int qp = 0; qp < 9; ++qp) {
+        const double w = c_simpson[qp];
+        double ul0, ul1, ul2, ul3, ul4, ur0, ur1, ur2, ur3, ur4;
+        rebuild_state(C, cl_, c_dplus[axis][qp], floor_, onepf, ul0, ul1, ul2, ul3, ul4);
+        asm volatile("" ::: "memory");  // bound the smem loads in flight (register pressure)
+        rebuild_state(C, cr_, c_dminus[axis][qp], floor_, onepf, ur0, ur1, ur2, ur3, ur4);
+        const uint32_t key = (kbase + qp) * 4;
+        if (err == 0xFFFFFFFFu) {
+            if (ul0 <= 0.0) err = ((key + 0) << 12) | (1u << 10) | (uint32_t)cl_;
+            else if (ur0 <= 0.0) err = ((key + 1) << 12) | (1u << 10) | (uint32_t)cr_;
+        }
+        const double invl = dvd(1.0, ul0);
+        const double vxl = mul(ul1, invl), vyl = mul(ul2, invl), vzl = mul(ul3, invl);
+        const double kel = mul(0.5, add(add(mul(ul1, vxl), mul(ul2, vyl)), mul(ul3, vzl)));
+        const double pl = mul(gm1, sub(ul4, kel));
+        const double invr = dvd(1.0, ur0);
+        const double vxr = mul(ur1, invr), vyr = mul(ur2, invr), vzr = mul(ur3, invr);
+        const double ker = mul(0.5, add(add(mul(ur1, vxr), mul(ur2, vyr)), mul(ur3, vzr)));
+        const double pr = mul(gm1, sub(ur4, ker));
+        if (err == 0xFFFFFFFFu) {
+            if (pl <= 0.0) err = ((key + 2) << 12) | (2u << 10) | (uint32_t)cl_;
+            else if (pr <= 0.0) err = ((key + 3) << 12) | (2u << 10) | (uint32_t)cr_;
+        }
+        const double cl = dsqrt(mul(mul(gamma, pl), invl));
+        const double cr = dsqrt(mul(mul(gamma, pr), invr));
+        const double vnl = axis == 0 ? vxl : (axis == 1 ? vyl : vzl);
+        const double vnr = axis == 0 ? vxr : (axis == 1 ? vyr : vzr);
+        const double sl = add(fabs(vnl), cl);
+        const double sr = add(fabs(vnr), cr);
+        const double s = sl > sr ? sl : sr;
+        if (s > smax) smax = s;
+        const double fl0 = mul(ul0, vnl);
+        double fl1 = mul(ul1, vnl), fl2 = mul(ul2, vnl), fl3 = mul(ul3, vnl);
+        const double fl4 = mul(add(ul4, pl), vnl);
+        const double fr0 = mul(ur0, vnr);
+        double fr1 = mul(ur1, vnr), fr2 = mul(ur2, vnr), fr3 = mul(ur3, vnr);
+        const double fr4 = mul(add(ur4, pr), vnr);
+        if (axis == 0) {
+            fl1 = add(fl1, pl);
+            fr1 = add(fr1, pr);
+        } else if (axis == 1) {
+            fl2 = add(fl2, pl);
+            fr2 = add(fr2, pr);
+        } else {
+            fl3 = add(fl3, pl);
+            fr3 = add(fr3, pr);
+        }
+        const double hs = mul(0.5, s);
+        f0 = add(f0, mul(w, sub(mul(0.5, add(fl0, fr0)), mul(hs, sub(ur0, ul0)))));
+        f1 = add(f1, mul(w, sub(mul(0.5, add(fl1, fr1)), mul(hs, sub(ur1, ul1)))));
+        f2 = add(f2, mul(w, sub(mul(0.5, add(fl2, fr2)), mul(hs, sub(ur2, ul2)))));
+        f3 = add(f3, mul(w, sub(mul(0.5, add(fl3, fr3)), mul(hs, sub(ur3, ul3)))));
+        f4 = add(f4, mul(w, sub(mul(0.5, add(fl4, fr4)), mul(hs, sub(ur4, ul4)))));
+    }
+    double* o;
+    if (axis == 0) o = FX + b * 5 * 576 + (i * 8 + j) * 9 + k;
+    else if (axis == 1) o = FY + b * 5 * 576 + (i * 9 + j) * 8 + k;
+    else o = FZ + b * 5 * 576 + (j * 8 + i) * 8 + k;
+    o[0] = f0;
+    o[576] = f1;
+    o[2 * 576] = f2;
+    o[3 * 576] = f3;
+    o[4 * 576] = f4;
+}
+
+// async copy of leaf b's 5 x 12^3 block (rows of 12 doubles = 6 x 16 B,
+// 16-B aligned because the padded row pitch and the leaf origin are even)
+__device__ __forceinline__ void prefetch_block(double* Us, const FieldView& uv, const int32_t* leaves, int64_t b) {
+    const double* u0 = leaf_origin(uv, leaves, b, 2);
+    for (int c = threadIdx.x; c < NVAR * 144 * 6; c += FUSED_THREADS) {
+        const int row = c / 6, part = c % 6;
+        const int v = row / 144, r = row % 144;
+        const double* src = u0 + v * uv.comp_stride + (r / 12) * uv.sz + (r % 12) * uv.sy + 2 * part;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(Us + row * 12 + 2 * part);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(FUSED_THREADS, 1)
+hydro_fused_kernel(FieldView uv, const int32_t* __restrict__ leaves, int64_t B, double floor_, double gamma,
+                   double* __restrict__ FX, double* __restrict__ FY, double* __restrict__ FZ,
+                   double* __restrict__ smax_out, uint32_t* __restrict__ err_out, uint32_t* __restrict__ latch) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* Us = reinterpret_cast<double*>(smem_raw);  // [5][12][12][12]
+    double* C = Us + NVAR * 1728;                       // [20][1000]
+    __shared__ unsigned long long s_smax;
+    __shared__ uint32_t s_err;
+    const int t = threadIdx.x;
+    const double gm1 = sub(gamma, 1.0);
+    const double onepf = add(1.0, floor_);
+    int64_t b = blockIdx.x;
+    if (b < B) prefetch_block(Us, uv, leaves, b);
+    for (; b < B; b += gridDim.x) {
+        if (t == 0) {
+            s_smax = 0ull;
+            s_err = 0xFFFFFFFFu;
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+        // per region cell: centre values and minmod slopes (compiled.py:55-72)
+        for (int cell = t; cell < REC_CELLS; cell += FUSED_THREADS) {
+            const int x = cell % NRC + 1, y = (cell / NRC) % NRC + 1, z = cell / (NRC * NRC) + 1;
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) {
+                const double* p = Us + v * 1728 + (z * 12 + y) * 12 + x;
+                const double u = p[0];
+                C[v * REC_CELLS + cell] = u;
+                C[(NVAR + v * 3 + 0) * REC_CELLS + cell] = minmod(sub(p[1], u), sub(u, p[-1]));
+                C[(NVAR + v * 3 + 1) * REC_CELLS + cell] = minmod(sub(p[12], u), sub(u, p[-12]));
+                C[(NVAR + v * 3 + 2) * REC_CELLS + cell] = minmod(sub(p[144], u), sub(u, p[-144]));
+            }
+        }
+        __syncthreads();
+        // the U block is consumed: stream the next leaf's in behind the faces
+        if (b + gridDim.x < B) prefetch_block(Us, uv, leaves, b + gridDim.x);
+        double smax = 0.0;
+        uint32_t err = 0xFFFFFFFFu;
+        // faces, axis-major; 576 = 18 warps per axis so the axis is warp-uniform
+#pragma unroll 1
+        for (int ff = t; ff < 3 * 576; ff += FUSED_THREADS)
+            fused_face(C, ff / 576, ff % 576, b, floor_, onepf, gamma, gm1, FX, FY, FZ, smax, err);
+        atomicMax(&s_smax, (unsigned long long)__double_as_longlong(smax));
+        if (err != 0xFFFFFFFFu) atomicMin(&s_err, err);
+        __syncthreads();
+        if (t == 0) {
+            smax_out[b] = __longlong_as_double((long long)s_smax);
+            err_out[b] = s_err;
+            if (latch && s_err != 0xFFFFFFFFu) atomicMin(latch + b, s_err);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // hydro update (in place on the U view) + the reference's checks
 // (kernels/__init__.py:168-187):  status = 0xFFFFFFFF ok, else
 //   kind<<16 | detail,  kind 0: dt<=0, 1: CFL, 2: rho<=0/NaN at cell, 3: E
@@ -383,6 +573,35 @@ int sg_flux(const double* Q, int64_t nleaves, double gamma, double* FX, double* 
     if (nleaves <= 0) return SG_OK;
     flux_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax, err, latch);
     return sg_check_launch("sg_flux");
+}
+
+int sg_hydro_fused(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+                   const int32_t* leaves, int64_t nleaves, double floor_, double gamma, double* FX, double* FY,
+                   double* FZ, double* smax, uint32_t* err, uint32_t* latch, void* stream) {
+    if (pad < 2) {
+        sg_set_error("sg_hydro_fused: U pad must be >= 2 (got %d)", pad);
+        return SG_EINVAL;
+    }
+    int rc = init_tables();
+    if (rc) return rc;
+    if (nleaves <= 0) return SG_OK;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(hydro_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM);
+        attr = true;
+    }
+    FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
+    if (((uintptr_t)U & 15) || (uv.sy & 1) || (uv.sz & 1) || (uv.comp_stride & 1) || (leaf_stride & 1)) {
+        sg_set_error("sg_hydro_fused: U rows must be 16-byte aligned (even pitches, aligned base)");
+        return SG_EINVAL;
+    }
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = nleaves < nsm ? nleaves : nsm;
+    hydro_fused_kernel<<<(unsigned)grid, FUSED_THREADS, FUSED_SMEM, (cudaStream_t)stream>>>(
+        uv, leaves, nleaves, floor_, gamma, FX, FY, FZ, smax, err, latch);
+    return sg_check_launch("sg_hydro_fused");
 }
 
 int sg_hydro_update(double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,

@@ -36,7 +36,7 @@ class UnigridState:
     """One rank's z-slab of a periodic level-L unigrid, resident on a GPU."""
 
     def __init__(self, level: int, hydro: HydroConfig | None = None, gravity: GravityConfig | None = None,
-                 slab: Slab | None = None, device=None, group=None):
+                 slab: Slab | None = None, device=None, group=None, fused_hydro: bool = True):
         B.require_device()
         self.level = level
         self.slab = slab or Slab(level)
@@ -64,7 +64,10 @@ class UnigridState:
         self.leaves = self.leaves_host.to(self.device)
         self.nleaves = len(self.leaves_host)
         nb = self.nleaves
-        self.Q = torch.empty((nb, 5, 26, 1000), **f64)
+        # fused reconstruct+flux never materialises Q; the unfused (drop-in
+        # kernel pair) path allocates it lazily
+        self.fused_hydro = fused_hydro
+        self._Q = None
         self.FX = torch.empty((nb, 5, 8, 8, 9), **f64)
         self.FY = torch.empty((nb, 5, 8, 9, 8), **f64)
         self.FZ = torch.empty((nb, 5, 9, 8, 8), **f64)
@@ -100,6 +103,12 @@ class UnigridState:
         for i, name in enumerate(("phi", "gx", "gy", "gz")):
             out[name] = g[i]
         return out
+
+    @property
+    def Q(self) -> torch.Tensor:
+        if self._Q is None:
+            self._Q = torch.empty((self.nleaves, 5, 26, 1000), dtype=torch.float64, device=self.device)
+        return self._Q
 
     def reset_errors(self) -> None:
         self.flux_latch.fill_(-1)
@@ -174,13 +183,19 @@ class UnigridState:
         self.hydro_kernels()
 
     def hydro_kernels(self) -> None:
-        ev = self._t("reconstruct")
-        B.reconstruct(self.U, self.uv, self.leaves, self.nleaves, self.h.positivity_floor, self.Q)
-        self._done(ev)
-        ev = self._t("flux")
-        B.flux(self.Q, self.nleaves, self.h.gamma, self.FX, self.FY, self.FZ, self.smax, self.flux_err,
-               self.flux_latch)
-        self._done(ev)
+        if self.fused_hydro:
+            ev = self._t("hydro_fused")
+            B.hydro_fused(self.U, self.uv, self.leaves, self.nleaves, self.h.positivity_floor, self.h.gamma,
+                          self.FX, self.FY, self.FZ, self.smax, self.flux_err, self.flux_latch)
+            self._done(ev)
+        else:
+            ev = self._t("reconstruct")
+            B.reconstruct(self.U, self.uv, self.leaves, self.nleaves, self.h.positivity_floor, self.Q)
+            self._done(ev)
+            ev = self._t("flux")
+            B.flux(self.Q, self.nleaves, self.h.gamma, self.FX, self.FY, self.FZ, self.smax, self.flux_err,
+                   self.flux_latch)
+            self._done(ev)
         ev = self._t("hydro_update")
         B.hydro_update(self.U, self.uv, self.leaves, self.nleaves, self.FX, self.FY, self.FZ, self.smax,
                        self.dt, 0.0, self.dx, self.h.cfl, self.upd_status, self.upd_latch)

@@ -305,3 +305,51 @@ def test_cfg5_slabs_match_golden(manifest, level, world):
     out = ls.fetch()
     for k in octree.HYDRO_FIELDS:
         assert digest(out[k]) == m["final_field_digests"][k], k
+
+
+def test_cfg4_hydro_fused_matches_golden(manifest):
+    """fused reconstruct+flux (no Q) == the reference's reconstruct -> flux."""
+    m = manifest["cfg4_hydro"]
+    gamma = float.fromhex(m["gamma"])
+    u = G.UnigridState(3, K.HydroConfig(gamma=gamma))
+    u.load(scenarios.config4_state(3))
+    u._halo(u.U, 5, u.uv)
+    B.hydro_fused(u.U, u.uv, u.leaves, u.nleaves, 1e-12, gamma, u.FX, u.FY, u.FZ, u.smax, u.flux_err)
+    assert (u.flux_err.cpu().numpy().view(np.uint32) == B.U32_OK).all()
+    FX, FY, FZ = u.FX.cpu().numpy(), u.FY.cpu().numpy(), u.FZ.cpu().numpy()
+    smax = u.smax.cpu().numpy()
+    for b, (cx, cy, cz) in enumerate(u.leaves_host.tolist()):
+        rec = m["leaves"]["%d,%d,%d" % (cx, cy, cz)]
+        assert digest(FX[b]) == rec["fx"] and digest(FY[b]) == rec["fy"] and digest(FZ[b]) == rec["fz"]
+        assert smax[b] == float.fromhex(rec["smax"])
+
+
+def test_fused_equals_unfused_on_random_and_poisoned_blocks():
+    g = load_npz("hydro_random.npz")
+    blocks = [g[f"U{i}"] for i in range(6)]
+    poisoned = blocks[0].copy()
+    poisoned[0, 6, 6, 1] = np.nan      # face ghost: must reach the interior
+    poisoned[4, 0, 0, 0] = np.nan      # corner: never read
+    blocks.append(poisoned)
+    U = dev(np.stack(blocks))
+    nb = len(blocks)
+    v = View(8, 8, 8, 2, leaf_stride=5 * 1728)
+    outs = []
+    for fused in (False, True):
+        FX = torch.empty((nb, 5, 8, 8, 9), dtype=torch.float64, device="cuda")
+        FY = torch.empty((nb, 5, 8, 9, 8), dtype=torch.float64, device="cuda")
+        FZ = torch.empty((nb, 5, 9, 8, 8), dtype=torch.float64, device="cuda")
+        smax = torch.empty(nb, dtype=torch.float64, device="cuda")
+        err = torch.empty(nb, dtype=torch.int32, device="cuda")
+        if fused:
+            B.hydro_fused(U, v, None, nb, 1e-12, 1.4, FX, FY, FZ, smax, err)
+        else:
+            Q = torch.empty((nb, 5, 26, 1000), dtype=torch.float64, device="cuda")
+            B.reconstruct(U, v, None, nb, 1e-12, Q)
+            B.flux(Q, nb, 1.4, FX, FY, FZ, smax, err)
+        outs.append([t.cpu().numpy() for t in (FX, FY, FZ, smax, err)])
+    for a, b in zip(*outs):
+        assert same(a, b)
+    assert np.isnan(outs[1][0][6]).any()
+    for i in range(6):
+        assert bitwise(outs[1][0][i], g[f"FX{i}"]) and bitwise(outs[1][2][i], g[f"FZ{i}"])

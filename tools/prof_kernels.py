@@ -24,7 +24,9 @@ if what in ("hydro", "all"):
     u = grid.UnigridState(level, HydroConfig(gamma=5.0 / 3.0))
     u.load(scenarios.config4_state(level))
     u.dt.fill_(1e-6)
-    for _ in range(2):
-        u.hydro_iteration()
+    for fused in (True, False):
+        u.fused_hydro = fused
+        for _ in range(2):
+            u.hydro_iteration()
 torch.cuda.synchronize()
 print("ok")
