@@ -56,7 +56,8 @@ def config_dict(world: int) -> dict:
     return {"workload": "config5: full timestep, 128^3 unigrid (4096 subgrids of 8^3), 6x(P2P+M2L) + 3x hydro",
             "level": LEVEL, "subgrids": 8 ** LEVEL, "theta": 0.34, "eps": 0.5, "expansion_order": 1,
             "gamma": 1.4, "floor": 0.05, "omega": 0.1, "parallelism": f"zslab{world}",
-            "l2": "per-step working set > L2 (Q buffer 4.26 GB/step); no explicit flush"}
+            "l2": "per-step working set > L2 (fluxes 283 MB written+read per hydro iteration, state 92 MB); "
+                  "no explicit flush"}
 
 
 # -- clocks ---------------------------------------------------------------------
@@ -161,7 +162,7 @@ def run_reference(args) -> None:
     kind = "port-native" if O.use_native() else "port"
     threads = O.max_threads()
     state = scenarios.config5_state(LEVEL)
-    m2l_leaves = max(2 * threads, 32)
+    m2l_leaves = max(16 * threads, 64)
     for _ in range(args.warmup):
         cpu_sample(state, LEVEL, threads, m2l_leaves)
     vals, steps = [], []
@@ -190,6 +191,23 @@ def run_reference(args) -> None:
 
 
 # -- our arm ------------------------------------------------------------------------
+
+def m2l_traffic_from_profile():
+    """dram__bytes_read.sum + dram__bytes_write.sum of one M2L launch at
+    level 4, from the committed ncu --set full summary (profiles/)."""
+    import re
+    for f in sorted((REPO / "profiles").glob("r*_m2l_L4_ncu_full.txt"), reverse=True):
+        txt = f.read_text()
+        vals = {}
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            m = re.search(key + r"\s+([0-9.]+)\s+(\w+)", txt)
+            if m:
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(m.group(2), 1)
+                vals[key] = float(m.group(1)) * scale
+        if len(vals) == 2:
+            return sum(vals.values()), f.name
+    return None, None
+
 
 def fp64_peak(torch) -> dict:
     import ctypes
@@ -308,8 +326,14 @@ def run_ours(args) -> None:
                 "peak": peaks["dfma_tflops"], "frac": achieved / peaks["dfma_tflops"],
                 "peak_source": "measured in this run: DFMA microbenchmark (sg_fp64_peak); FMA counted as 2 FLOP",
                 "peak_issue": peaks["dadd_tflops"], "frac_issue": achieved / peaks["dadd_tflops"],
-                "flop_per_subgrid": M2L_FLOP[1], "subgrids_per_launch": u.nleaves,
-                "traffic": None}
+                "flop_per_subgrid": M2L_FLOP[1], "subgrids_per_launch": u.nleaves}
+    traffic, src = m2l_traffic_from_profile()
+    roofline["traffic"] = traffic if u.nleaves == 4096 else None
+    roofline["traffic_unit"] = "bytes/launch (DRAM read+write, ncu)"
+    roofline["traffic_source"] = f"profiles/{src}" if src else None
+    roofline["note"] = ("FP64 CUDA-core bound (not hbm/tensor): parity forbids FMA contraction, so the "
+                        "attainable ceiling is the DADD/DMUL issue rate (frac_issue); traffic << algorithmic "
+                        "bytes because the neighbourhoods are re-read from L2")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -330,7 +354,7 @@ def run_ours(args) -> None:
             from oracle import oracle as O
             kind = "port-native" if O.use_native() else "port"
             threads = O.max_threads()
-            r = cpu_sample(state, LEVEL, threads, max(2 * threads, 32))
+            r = cpu_sample(state, LEVEL, threads, max(16 * threads, 64))
             line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
                                     "build": kind, "sample": r["sample"], "rates": r["rates"]}
         except Exception as exc:  # the baseline is a report, never the product
