@@ -234,8 +234,10 @@ class UnigridState:
         kind, detail = int(up[b]) >> 16, int(up[b]) & 0xFFFF
         if kind == 0:
             raise KernelError(f"{prefix}dt must be positive, got {self.dt.item()}")
-        if kind == 1:
-            raise KernelError(f"{prefix}CFL violation at leaf {coord}: dt={self.dt.item():g}")
+        if kind == 1:  # message of reference kernels/__init__.py:170-174
+            dt, smax = self.dt.item(), float(self.smax[b].item())
+            raise KernelError(f"{prefix}CFL violation: dt={dt:g} exceeds cfl*dx/s_max="
+                              f"{self.h.cfl * self.dx / smax:g} (s_max={smax:g})")
         name = "rho" if kind == 2 else "E"
         raise KernelError(f"{prefix}non-positive (or NaN) {name} after update at interior cell "
                           f"(x={detail % 8}, y={(detail // 8) % 8}, z={detail // 64}) of leaf {coord}")

@@ -363,6 +363,28 @@ def cfg5(man, level, gravity):
     }
 
 
+def scenario_runs(man):
+    """The reference's own driver.run_scenario (driver.py:91-189) end to end:
+    fields_bytes-style digests of the final tree (tests/util.py:66-67)."""
+    from simdgrid.driver import run_scenario
+    from simdgrid.scenarios import ScenarioConfig, init_scenario
+    names = ("rho", "sx", "sy", "sz", "E", "phi", "gx", "gy", "gz")
+    rec = {}
+    for name, level, steps in (("rotating-star-proxy", 1, 2), ("blast", 1, 3), ("rotating-star-proxy", 2, 1)):
+        cfg = ScenarioConfig(name, max_level=level, stop_step=steps)
+        init = init_scenario(cfg)
+        res = run_scenario(cfg, backend="scalar", threads=os.cpu_count() or 4)
+        fb = b"".join(leaf.interior(n).tobytes() for leaf in res.tree.leaves for n in names)
+        rec[f"{name}_L{level}_s{steps}"] = {
+            "level": level, "steps": steps,
+            "input_digests": {n: digest(global_from_tree(init, n)) for n in FIELDS + ("mass",)},
+            "fields_bytes_sha256": hashlib.sha256(fb).hexdigest(),
+            "field_digests": {n: digest(global_from_tree(res.tree, n)) for n in names + ("mass",)},
+            "counts": {r.name: r.count for r in res.records},
+        }
+    man["scenarios"] = rec
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-l4", action="store_true")
@@ -371,7 +393,7 @@ def main():
     man_path = HERE / "manifest.json"
     man = json.loads(man_path.read_text()) if man_path.exists() else {}
     todo = args.only.split(",") if args.only else [
-        "cfg1", "tree", "hydro_random", "cfg2", "cfg4", "cfg3", "cfg5_L2", "cfg5_L4"]
+        "cfg1", "tree", "hydro_random", "cfg2", "cfg4", "cfg3", "cfg5_L2", "cfg5_L4", "scenarios"]
     for name in todo:
         if name == "cfg5_L4" and args.skip_l4:
             continue
@@ -380,7 +402,8 @@ def main():
         {"cfg1": lambda: gravity_cfg1(), "tree": lambda: gravity_tree(),
          "hydro_random": lambda: hydro_random(), "cfg2": lambda: cfg2_p2p(man),
          "cfg3": lambda: cfg3_m2l(man), "cfg4": lambda: cfg4_hydro(man),
-         "cfg5_L2": lambda: cfg5(man, 2, "every"), "cfg5_L4": lambda: cfg5(man, 4, "last")}[name]()
+         "cfg5_L2": lambda: cfg5(man, 2, "every"), "cfg5_L4": lambda: cfg5(man, 4, "last"),
+         "scenarios": lambda: scenario_runs(man)}[name]()
         man["_generator"] = "tests/golden/make_golden.py (reference simdgrid, numba compiled path)"
         man_path.write_text(json.dumps(man, indent=1, sort_keys=True))
         print(f"[golden] {name} done in {time.time() - t0:.1f}s", flush=True)

@@ -1,0 +1,45 @@
+"""run_scenario on the B200 backend vs the reference's own run_scenario
+(golden: tests/golden/manifest.json "scenarios")."""
+
+from __future__ import annotations
+
+import hashlib
+
+import pytest
+
+from conftest import digest
+
+pytestmark = pytest.mark.gpu
+
+from paper_2210_06439_b200 import driver as D  # noqa: E402
+from paper_2210_06439_b200.octree import global_field  # noqa: E402
+
+NAMES = ("rho", "sx", "sy", "sz", "E", "phi", "gx", "gy", "gz")
+
+
+@pytest.mark.parametrize("key", ["rotating-star-proxy_L1_s2", "blast_L1_s3", "rotating-star-proxy_L2_s1"])
+def test_run_scenario_matches_reference(manifest, key):
+    rec = manifest["scenarios"][key]
+    name = key.rsplit("_L", 1)[0]
+    cfg = D.ScenarioConfig(name, max_level=rec["level"], stop_step=rec["steps"])
+    init = D.init_scenario(cfg)
+    if any(digest(global_field(init, f)) != d for f, d in rec["input_digests"].items()):
+        pytest.skip("scenario ICs differ on this host (numpy SIMD transcendentals)")
+    res = D.run_scenario(cfg, backend="emulated8")
+    for f, d in rec["field_digests"].items():
+        assert digest(global_field(res.tree, f)) == d, f
+    fb = b"".join(leaf.interior(n).tobytes() for leaf in res.tree.leaves for n in NAMES)
+    assert hashlib.sha256(fb).hexdigest() == rec["fields_bytes_sha256"]
+    counts = {r.name: r.count for r in res.records}
+    assert counts == rec["counts"]
+    assert res.computation_s > 0 and res.launch_stats.gpu_launches > 0
+
+
+def test_sweep_csv(tmp_path):
+    cfg = D.ScenarioConfig("blast", max_level=0, stop_step=1)
+    path = tmp_path / "sweep.csv"
+    rows = D.sweep(cfg, [1, 2], ["scalar", "emulated4"], str(path))
+    assert len(rows) == D.expected_row_count("blast", 4)
+    text = path.read_text(encoding="utf-8")
+    assert text.startswith(D.CSV_HEADER)
+    assert sum(1 for ln in text.strip().split("\n")[1:] if ",total," in ln) == 4
