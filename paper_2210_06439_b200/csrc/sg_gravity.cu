@@ -14,6 +14,8 @@
 // only the data-dependent DADD/DMUL stream.  Masked (+0.0) terms and the
 // unselected far/near branch are skipped: accumulators start at +0.0 and are
 // never -0.0, so skipping x + 0.0 is exact.
+#include <cmath>
+
 #include "sg_common.cuh"
 #include "../../include/sg.h"
 
@@ -52,6 +54,16 @@ struct P2PEntry {
 };
 
 constexpr int P2P_THREADS = 512;
+// halo <= 2 (theta >= 1/3, incl. the benchmark's 0.34): the compacted stencil
+// rides in the kernel-parameter constant bank -- uniform across the warp, so
+// it costs no shared-memory bandwidth (the smem-staged path was LDS-bound)
+constexpr int P2P_PARAM_MAX = 124;
+struct P2PStencil {
+    int count;
+    int pad_;
+    double rx[P2P_PARAM_MAX], ry[P2P_PARAM_MAX], rz[P2P_PARAM_MAX], inv[P2P_PARAM_MAX], inv3[P2P_PARAM_MAX];
+    int delta[P2P_PARAM_MAX];
+};
 
 __host__ __device__ inline int p2p_pitch(int S) {
     // row pitch (doubles) == 8 (mod 16): the two y-rows of a half-warp land on
@@ -105,7 +117,60 @@ __device__ int p2p_build_chunk(P2PEntry* ent, int* warp_cnt, int c0, int halo, d
     return cnt;
 }
 
-__global__ void __launch_bounds__(P2P_THREADS, 1)
+// two targets per thread, (x, y, z) and (x, y, z + 4): each uniform stencil
+// entry is loaded once for both (the kernel is issue-bound)
+constexpr int P2P_PARAM_THREADS = 256;
+__global__ void __launch_bounds__(P2P_PARAM_THREADS, 4)
+p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, int halo, FieldView ov,
+                 const __grid_constant__ P2PStencil st) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int S = NIN + 2 * halo;
+    const int pitch = p2p_pitch(S);
+    const int plane = pitch * S;
+    double* cube = reinterpret_cast<double*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;  // z in 0..3; second target z + 4
+    const int tcell = (z + halo) * plane + (y + halo) * pitch + (x + halo);
+    const int t2 = tcell + 4 * plane;
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        __syncthreads();
+        const double* src = leaf_origin(mv, leaves, b, halo);
+        for (int i = tid; i < S * S * S; i += P2P_PARAM_THREADS) {
+            const int cx = i % S, cy = (i / S) % S, cz = i / (S * S);
+            cube[cz * plane + cy * pitch + cx] = __ldg(src + cz * mv.sz + cy * mv.sy + cx);
+        }
+        __syncthreads();
+        double ap = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
+        double bp = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+#pragma unroll 4
+        for (int e = 0; e < st.count; ++e) {
+            const int d = st.delta[e];
+            const double inv = st.inv[e], inv3 = st.inv3[e], rx = st.rx[e], ry = st.ry[e], rz = st.rz[e];
+            const double ma = cube[tcell + d], mb = cube[t2 + d];
+            const double ca = mul(ma, inv3), cb = mul(mb, inv3);
+            ap = add(ap, -mul(ma, inv));
+            ax = add(ax, -mul(ca, rx));
+            ay = add(ay, -mul(ca, ry));
+            az = add(az, -mul(ca, rz));
+            bp = add(bp, -mul(mb, inv));
+            bx = add(bx, -mul(cb, rx));
+            by = add(by, -mul(cb, ry));
+            bz = add(bz, -mul(cb, rz));
+        }
+        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy + x;
+        o[0] = ap;
+        o[ov.comp_stride] = ax;
+        o[2 * ov.comp_stride] = ay;
+        o[3 * ov.comp_stride] = az;
+        o += 4 * ov.sz;
+        o[0] = bp;
+        o[ov.comp_stride] = bx;
+        o[2 * ov.comp_stride] = by;
+        o[3 * ov.comp_stride] = bz;
+    }
+}
+
+__global__ void __launch_bounds__(P2P_THREADS, 2)
 p2p_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, double dx, double rad2,
            double eps2, int halo, FieldView ov, double* __restrict__ out_base) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -516,10 +581,49 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     FieldView mv = make_view(mass, nx, ny, nz, pad, leaf_stride);
     FieldView ov = make_view(out, onx, ony, onz, 0, out_leaf_stride);
     const int S = NIN + 2 * halo;
+    const int64_t grid = nleaves < 2 * sm_count() ? nleaves : 2 * sm_count();
+    if (halo <= 2) {
+        // host-built stencil: compiled.py:299-313 with the same IEEE-rounded
+        // ops (host code is built with -ffp-contract=off), offsets in
+        // (oz, oy, ox) lexicographic order, masked ones dropped
+        static thread_local P2PStencil st;
+        const int pitch = p2p_pitch(S), plane = pitch * S;
+        st.count = 0;
+        for (int oz = -halo; oz <= halo; ++oz) {
+            volatile double rz = (-(double)oz) * dx;
+            for (int oy = -halo; oy <= halo; ++oy) {
+                volatile double ry = (-(double)oy) * dx;
+                for (int ox = -halo; ox <= halo; ++ox) {
+                    volatile double rx = (-(double)ox) * dx;
+                    volatile double rxx = rx * rx, ryy = ry * ry, rzz = rz * rz;
+                    volatile double s1 = rxx + ryy;
+                    volatile double r2 = s1 + rzz;
+                    if (!(r2 <= rad2) || (ox == 0 && oy == 0 && oz == 0)) continue;
+                    volatile double r2e = r2 + eps2;
+                    volatile double rt = std::sqrt((double)r2e);
+                    volatile double inv = 1.0 / rt;
+                    volatile double inv2 = inv * inv;
+                    volatile double inv3 = inv2 * inv;
+                    const int e = st.count++;
+                    st.rx[e] = rx;
+                    st.ry[e] = ry;
+                    st.rz[e] = rz;
+                    st.inv[e] = inv;
+                    st.inv3[e] = inv3;
+                    st.delta[e] = oz * plane + oy * pitch + ox;
+                }
+            }
+        }
+        const size_t smem = sizeof(double) * (size_t)S * S * p2p_pitch(S);
+        cudaFuncSetAttribute(p2p_param_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t pgrid = nleaves < 4 * sm_count() ? nleaves : 4 * sm_count();
+        p2p_param_kernel<<<(unsigned)pgrid, P2P_PARAM_THREADS, smem, (cudaStream_t)stream>>>(mv, leaves, nleaves,
+                                                                                              halo, ov, st);
+        return sg_check_launch("sg_p2p");
+    }
     const size_t smem = sizeof(P2PEntry) * P2P_THREADS + sizeof(int) * 32 +
                         sizeof(double) * (size_t)S * S * p2p_pitch(S);
     cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int64_t grid = nleaves < 2 * sm_count() ? nleaves : 2 * sm_count();
     p2p_kernel<<<(unsigned)grid, P2P_THREADS, smem, (cudaStream_t)stream>>>(
         mv, leaves, nleaves, dx, rad2, eps2, halo, ov, out);
     return sg_check_launch("sg_p2p");

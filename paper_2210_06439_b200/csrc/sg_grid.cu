@@ -29,33 +29,53 @@ int sg_check_launch(const char* what) {
 namespace sg {
 
 // Fill the pad cells of `ncomp` padded fields (dims (nz+2p, ny+2p, nx+2p))
-// from the periodic image of the interior.  Axes not in wrap_mask (bit0 x,
-// bit1 y, bit2 z) are left untouched in their pad range: the z-slab halo
-// exchange fills those planes from the neighbouring rank.
+// from the periodic image of the interior.  Only pad cells get a thread: the
+// flat index runs over region A (the 2p z-pad planes, whole), B (interior z,
+// the 2p y-pad rows) and C (interior z and y, the 2p x-pad cells).  Every
+// out-of-range axis in wrap_mask (bit0 x, bit1 y, bit2 z) maps to its
+// periodic image, so sources are interior cells along wrapped axes and the
+// fill has no read/write overlap.  A non-wrapped axis keeps its coordinate:
+// in z-slab mode (mask 3) region A is skipped -- those planes arrive whole
+// from the neighbour ranks after this fill.
 __global__ void fill_periodic_kernel(double* __restrict__ f, int64_t ncomp, int64_t nx, int64_t ny,
                                      int64_t nz, int pad, int wrap_mask) {
     const int64_t X = nx + 2 * pad, Y = ny + 2 * pad, Z = nz + 2 * pad;
     const int64_t vol = X * Y * Z;
+    const bool wz = wrap_mask & 4;
+    const int64_t nA = wz ? 2 * pad * Y * X : 0, nB = nz * 2 * pad * X, nC = nz * ny * 2 * pad;
+    const int64_t per = nA + nB + nC;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= vol * ncomp) return;
-    const int64_t c = i / vol, r = i % vol;
-    const int64_t x = r % X, y = (r / X) % Y, z = r / (X * Y);
-    const bool ix = x >= pad && x < pad + nx, iy = y >= pad && y < pad + ny, iz = z >= pad && z < pad + nz;
-    if (ix && iy && iz) return;
+    if (i >= per * ncomp) return;
+    const int64_t c = i / per;
+    int64_t r = i % per, x, y, z;
+    if (r < nA) {
+        x = r % X;
+        y = (r / X) % Y;
+        const int64_t zp = r / (X * Y);
+        z = zp < pad ? zp : nz + zp;
+    } else if ((r -= nA) < nB) {
+        x = r % X;
+        const int64_t yp = (r / X) % (2 * pad);
+        y = yp < pad ? yp : ny + yp;
+        z = pad + r / (X * 2 * pad);
+    } else {
+        r -= nB;
+        const int64_t xp = r % (2 * pad);
+        x = xp < pad ? xp : nx + xp;
+        y = pad + (r / (2 * pad)) % ny;
+        z = pad + r / (2 * pad * ny);
+    }
     auto wrapc = [pad](int64_t v, int64_t n) {
         int64_t w = (v - pad) % n;
         if (w < 0) w += n;
         return w + pad;
     };
-    // wrapped axes map to their periodic image; a non-wrapped axis keeps its
-    // coordinate (its halo planes are filled externally, then their x/y pads
-    // are wrapped here within the same plane).  Sources are never pad cells
-    // of a wrapped axis, so the fill has no read/write overlap.
+    const bool ix = x >= pad && x < pad + nx, iy = y >= pad && y < pad + ny, iz = z >= pad && z < pad + nz;
     const int64_t sx = (!ix && (wrap_mask & 1)) ? wrapc(x, nx) : x;
     const int64_t sy = (!iy && (wrap_mask & 2)) ? wrapc(y, ny) : y;
-    const int64_t sz = (!iz && (wrap_mask & 4)) ? wrapc(z, nz) : z;
+    const int64_t sz = (!iz && wz) ? wrapc(z, nz) : z;
     if (sx == x && sy == y && sz == z) return;
-    f[i] = f[c * vol + (sz * Y + sy) * X + sx];
+    f[c * vol + (z * Y + y) * X + x] = f[c * vol + (sz * Y + sy) * X + sx];
 }
 
 // dst interior (pad pd) = src interior (pad ps, component 0) * scale
@@ -92,7 +112,9 @@ int sg_fill_periodic(double* field, int64_t ncomp, int64_t nx, int64_t ny, int64
                      (long long)nx, (long long)ny, (long long)nz);
         return SG_EINVAL;
     }
-    const int64_t total = (nx + 2 * pad) * (ny + 2 * pad) * (nz + 2 * pad) * ncomp;
+    const int64_t X = nx + 2 * pad, Y = ny + 2 * pad;
+    const int64_t per = ((wrap_mask & 4) ? 2 * pad * Y * X : 0) + nz * 2 * pad * X + nz * ny * 2 * pad;
+    const int64_t total = per * ncomp;
     if (total == 0 || pad == 0) return SG_OK;
     fill_periodic_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         field, ncomp, nx, ny, nz, pad, wrap_mask);
