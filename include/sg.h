@@ -139,6 +139,13 @@ int sg_dt_from_smax(const double *s_pre, double cfl, double dx, double *dt, void
 int sg_fill_periodic(double *field, int64_t ncomp, int64_t nx, int64_t ny, int64_t nz, int32_t pad,
                      int32_t wrap_mask, void *stream);
 
+/* Batched octree.source_cube (octree.py:186-214) / ghost-filled 12^3 blocks:
+ * out[b][c][z][y][x] for the (8+2*halo)^3 box around leaf b's interior,
+ * from any field view with pad >= halo (pads filled). */
+int sg_gather_blocks(const double *field, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+                     const int32_t *leaves, int64_t nleaves, int64_t ncomp, int32_t halo, double *out,
+                     void *stream);
+
 /* driver.py:165-166: dst interior (pad dst_pad) = src component 0 interior
  * (pad src_pad) * scale, with scale = dx**3. */
 int sg_scale_copy(double *dst, int32_t dst_pad, const double *src, int32_t src_pad, int64_t nx, int64_t ny,

@@ -36,6 +36,7 @@ SIGNATURES = {
     "sg_max_reduce": [_p, _i64, _p, _p],
     "sg_dt_from_smax": [_p, _d, _d, _p, _p],
     "sg_fill_periodic": [_p, _i64, _i64, _i64, _i64, _i32, _i32, _p],
+    "sg_gather_blocks": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _i64, _i32, _p, _p],
     "sg_scale_copy": [_p, _i32, _p, _i32, _i64, _i64, _i64, _d, _p],
     "sg_fp64_peak": [ctypes.c_int, ctypes.c_int, _p, ctypes.POINTER(_i64), _p],
 }

@@ -144,3 +144,9 @@ def fill_periodic(field, ncomp: int, v: View, wrap_mask: int = 7) -> None:
 
 def scale_copy(dst, dst_pad: int, src, src_pad: int, nx: int, ny: int, nz: int, scale: float) -> None:
     _lib.call("sg_scale_copy", _f64(dst), dst_pad, _f64(src), src_pad, nx, ny, nz, float(scale), _stream())
+
+
+def gather_blocks(field, v: View, leaves, nleaves: int, ncomp: int, halo: int, out) -> None:
+    """out[b, c] = the (8+2*halo)^3 box around leaf b (batched source_cube)."""
+    _lib.call("sg_gather_blocks", _f64(field), v.nx, v.ny, v.nz, v.pad, v.leaf_stride, _ptr(leaves), nleaves,
+              int(ncomp), int(halo), _f64(out), _stream())

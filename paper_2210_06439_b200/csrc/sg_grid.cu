@@ -88,6 +88,21 @@ __global__ void scale_copy_kernel(double* __restrict__ dst, int pd, const double
     dst[((z + pd) * Yd + (y + pd)) * Xd + (x + pd)] = mul(src[((z + ps) * Ys + (y + ps)) * Xs + (x + ps)], scale);
 }
 
+// out[b][c][z][y][x] = field(b, c, origin - halo + (z, y, x)) for z,y,x in
+// [0, 8 + 2*halo): the batched octree.source_cube (octree.py:186-214) on a
+// padded device field
+__global__ void gather_blocks_kernel(FieldView v, const int32_t* __restrict__ leaves, int64_t nleaves,
+                                     int64_t ncomp, int halo, double* __restrict__ out) {
+    const int S = NIN + 2 * halo;
+    const int64_t per = (int64_t)S * S * S;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= per * ncomp * nleaves) return;
+    const int64_t b = i / (per * ncomp), r = i % (per * ncomp);
+    const int64_t c = r / per, e = r % per;
+    const int x = e % S, y = (e / S) % S, z = e / (S * S);
+    out[i] = leaf_origin(v, leaves, b, halo)[c * v.comp_stride + z * v.sz + y * v.sy + x];
+}
+
 }  // namespace sg
 
 using namespace sg;
@@ -119,6 +134,22 @@ int sg_fill_periodic(double* field, int64_t ncomp, int64_t nx, int64_t ny, int64
     fill_periodic_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         field, ncomp, nx, ny, nz, pad, wrap_mask);
     return sg_check_launch("sg_fill_periodic");
+}
+
+int sg_gather_blocks(const double* field, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
+                     const int32_t* leaves, int64_t nleaves, int64_t ncomp, int32_t halo, double* out,
+                     void* stream) {
+    if (halo < 0 || halo > pad) {
+        sg_set_error("sg_gather_blocks: halo %d must be in [0, pad=%d]", halo, pad);
+        return SG_EINVAL;
+    }
+    const int S = NIN + 2 * halo;
+    const int64_t total = (int64_t)S * S * S * ncomp * nleaves;
+    if (total == 0) return SG_OK;
+    FieldView v = make_view(field, nx, ny, nz, pad, leaf_stride);
+    gather_blocks_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(v, leaves, nleaves,
+                                                                                            ncomp, halo, out);
+    return sg_check_launch("sg_gather_blocks");
 }
 
 int sg_scale_copy(double* dst, int32_t dst_pad, const double* src, int32_t src_pad, int64_t nx, int64_t ny,

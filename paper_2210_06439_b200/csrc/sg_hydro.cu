@@ -585,11 +585,7 @@ int sg_hydro_fused(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
     int rc = init_tables();
     if (rc) return rc;
     if (nleaves <= 0) return SG_OK;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(hydro_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM);
-        attr = true;
-    }
+    cudaFuncSetAttribute(hydro_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM);
     FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
     if (((uintptr_t)U & 15) || (uv.sy & 1) || (uv.sz & 1) || (uv.comp_stride & 1) || (leaf_stride & 1)) {
         sg_set_error("sg_hydro_fused: U rows must be 16-byte aligned (even pitches, aligned base)");

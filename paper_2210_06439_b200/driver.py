@@ -219,9 +219,10 @@ def run_scenario(cfg: ScenarioConfig, backend: str = "scalar", threads: int = 1,
         c, t = recs.get(name, (0, 0))
         recs[name] = (c + len(evs) * st.nleaves, t + ns)
     records = tuple(ProfileRecord(n, c, t) for n, (c, t) in recs.items()) + (ProfileRecord("total", 1, total_ns),)
-    if profiler is not None and hasattr(profiler, "_add"):
+    if profiler is not None:
+        # a profiling.CudaProfiler (or anything with add(name, count, total_ns))
         for r in records:
-            profiler._add(r.name, r.total_ns)
+            profiler.add(r.name, r.count, r.total_ns)
 
     out = st.fetch()
     for name in HYDRO_FIELDS + ("phi", "gx", "gy", "gz"):

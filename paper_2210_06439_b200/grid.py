@@ -110,6 +110,43 @@ class UnigridState:
             self._Q = torch.empty((self.nleaves, 5, 26, 1000), dtype=torch.float64, device=self.device)
         return self._Q
 
+    # -- octree <-> device ------------------------------
+
+    @classmethod
+    def from_tree(cls, tree, hydro: HydroConfig | None = None, gravity: GravityConfig | None = None,
+                  **kw) -> "UnigridState":
+        """Device-resident state of a (reference or local) unigrid Octree: the
+        leaves' interiors become the padded global fields."""
+        from .octree import global_field
+        st = cls(tree.max_level, hydro, gravity, **kw)
+        st.load({name: global_field(tree, name) for name in HYDRO_FIELDS})
+        return st
+
+    def to_tree(self, tree, names=HYDRO_FIELDS + ("phi", "gx", "gy", "gz")) -> None:
+        """Write the device state back into the tree's leaf interiors."""
+        from .octree import set_global_field
+        if self.slab.world != 1:
+            raise ValueError("to_tree needs the whole domain (single slab)")
+        out = self.fetch()
+        for name in names:
+            set_global_field(tree, name, out[name])
+
+    def source_cubes(self, field: str = "mass", halo: int = 8, leaf_ids=None) -> torch.Tensor:
+        """Batched octree.source_cube on the device: (B, 8+2h, 8+2h, 8+2h)
+        boxes of `mass` (pad 8) or of a hydro variable (pad 2), after the
+        periodic fill.  leaf_ids index self.leaves (default: all)."""
+        if field == "mass":
+            f, v, ncomp = self.mass, self.mv, 1
+        else:
+            f, v, ncomp = self.U[HYDRO_FIELDS.index(field)], self.uv, 1
+        self._halo(f.view((ncomp,) + v.padded_shape), ncomp, v)
+        leaves = self.leaves if leaf_ids is None else self.leaves[torch.as_tensor(leaf_ids, device=self.device)]
+        leaves = leaves.contiguous()
+        S = 8 + 2 * halo
+        out = torch.empty((len(leaves), S, S, S), dtype=torch.float64, device=self.device)
+        B.gather_blocks(f, v, leaves, len(leaves), 1, halo, out)
+        return out
+
     def reset_errors(self) -> None:
         self.flux_latch.fill_(-1)
         self.upd_latch.fill_(-1)

@@ -43,3 +43,42 @@ def test_sweep_csv(tmp_path):
     text = path.read_text(encoding="utf-8")
     assert text.startswith(D.CSV_HEADER)
     assert sum(1 for ln in text.strip().split("\n")[1:] if ",total," in ln) == 4
+
+
+def test_cuda_profiler_and_device_source_cubes():
+    """8(f) rows 3-4: device source_cube batches match the host octree's,
+    and the CUDA-event profiler reports records in the reference format."""
+    import numpy as np
+    import torch
+
+    from paper_2210_06439_b200 import grid
+    from paper_2210_06439_b200.octree import neighborhood27, source_cube
+    from paper_2210_06439_b200.profiling import CudaProfiler
+
+    cfg = D.ScenarioConfig("rotating-star-proxy", max_level=1, stop_step=1)
+    tree = D.init_scenario(cfg)
+    st = grid.UnigridState.from_tree(tree, cfg.hydro, cfg.gravity)
+    st.set_mass()
+    cubes = st.source_cubes("mass", 8).cpu().numpy()
+    coords = [tuple(c) for c in st.leaves_host.tolist()]
+    for b, c in enumerate(coords):
+        lid = tree.leaf_id(c)
+        want = source_cube(neighborhood27(tree, lid), "mass", 8)
+        assert np.array_equal(cubes[b], want), c
+    rho2 = st.source_cubes("rho", 2).cpu().numpy()
+    for b, c in enumerate(coords):
+        want = source_cube(neighborhood27(tree, tree.leaf_id(c)), "rho", 2)
+        assert np.array_equal(rho2[b], want)
+    prof = CudaProfiler()
+    prof.timed("multipole", lambda: st.gravity_iteration(), weight=st.nleaves)
+    with prof.region("hydro", weight=st.nleaves):
+        st.wavespeed_dt()
+        st.hydro_iteration()
+    recs = {r.name: r for r in prof.report()}
+    assert recs["multipole"].count == 8 and recs["multipole"].total_ns > 0 and recs["hydro"].mean_ns > 0
+    res = D.run_scenario(cfg, profiler=prof)
+    assert prof.total_ns("total") == [r for r in res.records if r.name == "total"][0].total_ns
+    before = {n: tree.leaves[0].interior(n).copy() for n in ("rho", "phi")}
+    st.to_tree(tree)
+    assert not np.array_equal(tree.leaves[0].interior("phi"), before["phi"])  # gravity written back
+    assert torch.cuda.is_available()
