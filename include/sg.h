@@ -98,6 +98,13 @@ int sg_reconstruct(const double *U, int64_t nx, int64_t ny, int64_t nz, int32_t 
 int sg_flux(const double *Q, int64_t nleaves, double gamma, double *FX, double *FY, double *FZ,
             double *smax, uint32_t *err, uint32_t *latch, void *stream);
 
+/* Replaces the legacy straight-line flux (kernels/legacy.py:63-146; the
+ * reference's legacy reconstruct is value-identical to reconstruct_kernel).
+ * Outputs as sg_flux; err packs ((((axis*8+i)*9+j)*9+k)*9+q)*2 + check with
+ * the LEFT cell, the legacy kernel's convention. */
+int sg_flux_legacy(const double *Q, int64_t nleaves, double gamma, double *FX, double *FY, double *FZ,
+                   double *smax, uint32_t *err, uint32_t *latch, void *stream);
+
 /* Fused reconstruct + flux for the batched step: same outputs, smax, err and
  * latch as sg_reconstruct followed by sg_flux (bit-identical), without
  * materialising Q.  U view as sg_reconstruct. */

@@ -29,6 +29,7 @@ SIGNATURES = {
     "sg_m2l_workspace_bytes": [_i64],
     "sg_reconstruct": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _p, _p],
     "sg_flux": [_p, _i64, _d, _p, _p, _p, _p, _p, _p, _p],
+    "sg_flux_legacy": [_p, _i64, _d, _p, _p, _p, _p, _p, _p, _p],
     "sg_hydro_fused": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _d, _p, _p, _p, _p, _p, _p, _p],
     "sg_hydro_update": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _p, _p, _p, _p, _p, _d, _d, _d,
                         _p, _p, _p],

@@ -110,6 +110,12 @@ def flux(Q, nleaves: int, gamma: float, FX, FY, FZ, smax, err, latch=None) -> No
               _ptr(err), _ptr(latch), _stream())
 
 
+def flux_legacy(Q, nleaves: int, gamma: float, FX, FY, FZ, smax, err, latch=None) -> None:
+    """reference kernels/legacy.py flux formulation (not bitwise to flux())."""
+    _lib.call("sg_flux_legacy", _f64(Q), nleaves, float(gamma), _f64(FX), _f64(FY), _f64(FZ), _f64(smax),
+              _ptr(err), _ptr(latch), _stream())
+
+
 def hydro_fused(U, uv: View, leaves, nleaves: int, floor: float, gamma: float, FX, FY, FZ, smax, err,
                 latch=None) -> None:
     """reconstruct + flux without materialising Q (bit-identical outputs)."""

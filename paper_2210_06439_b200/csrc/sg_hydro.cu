@@ -253,6 +253,114 @@ flux_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX,
 }
 
 // ---------------------------------------------------------------------------
+// legacy flux (reference kernels/legacy.py:63-146): the old straight-line
+// formulation -- ke = |s|^2/(2 rho), v_n = s_n/rho, sqrt(gamma p / rho),
+// s = max(.,.) with Python semantics, and the first error always naming the
+// LEFT cell.  Physics-equal to flux_kernel, bit-identical to legacy.py.
+// The reference recomputes every quadrature state once per variable; the
+// values do not depend on v, so they are computed once per point here and
+// the five per-variable chains (each in (i1, i2) order) advance together.
+// err key = ((((axis*8+i)*9+j)*9+k)*9+q)*2 + check.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(FLUX_THREADS)
+flux_legacy_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX, double* __restrict__ FY,
+                   double* __restrict__ FZ, double* __restrict__ smax_out, uint32_t* __restrict__ err_out,
+                   uint32_t* __restrict__ latch) {
+    __shared__ unsigned long long s_smax;
+    __shared__ uint32_t s_err;
+    const int64_t b = blockIdx.x;
+    const int t = threadIdx.x;
+    if (t == 0) {
+        s_smax = 0ull;
+        s_err = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    const double* Qb = Q + b * (int64_t)(NVAR * NDIR * REC_CELLS);
+    const int64_t VS = (int64_t)NDIR * REC_CELLS;
+    const double gm1 = sub(gamma, 1.0);
+    double smax = 0.0;
+    uint32_t err = 0xFFFFFFFFu;
+#pragma unroll 1
+    for (int axis = 0; axis < 3; ++axis) {
+        const int nj = axis == 0 ? NIN : NIN + 1;
+        const int nk = axis == 0 ? NIN + 1 : NIN;
+        const int k = t % nk, j = (t / nk) % nj, i = t / (nk * nj);
+        int zl, zr, yl, yr, xl, xr;
+        if (axis == 0) {
+            zl = zr = i + 1; yl = yr = j + 1; xl = k; xr = k + 1;
+        } else if (axis == 1) {
+            zl = zr = i + 1; yl = j; yr = j + 1; xl = xr = k + 1;
+        } else {
+            zl = j; zr = j + 1; yl = yr = i + 1; xl = xr = k + 1;
+        }
+        const int cl_ = (zl * NRC + yl) * NRC + xl, cr_ = (zr * NRC + yr) * NRC + xr;
+        const uint32_t kbase = (uint32_t)((((axis * 8 + i) * 9 + j) * 9 + k) * 9);
+        double acc[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+        for (int qp = 0; qp < 9; ++qp) {
+            const double w = c_simpson[qp];
+            const double* pl_ = Qb + c_dplus[axis][qp] * REC_CELLS + cl_;
+            const double* pr_ = Qb + c_dminus[axis][qp] * REC_CELLS + cr_;
+            double ql[NVAR], qr[NVAR];
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) {
+                ql[v] = __ldg(pl_ + v * VS);
+                qr[v] = __ldg(pr_ + v * VS);
+            }
+            const double rl = ql[0], rr = qr[0];
+            const uint32_t key = (kbase + qp) * 2;
+            if (err == 0xFFFFFFFFu && (rl <= 0.0 || rr <= 0.0)) err = ((key + 0) << 12) | (1u << 10) | (uint32_t)cl_;
+            const double kel = dvd(add(add(mul(ql[1], ql[1]), mul(ql[2], ql[2])), mul(ql[3], ql[3])), mul(2.0, rl));
+            const double ker = dvd(add(add(mul(qr[1], qr[1]), mul(qr[2], qr[2])), mul(qr[3], qr[3])), mul(2.0, rr));
+            const double pl = mul(gm1, sub(ql[4], kel));
+            const double pr = mul(gm1, sub(qr[4], ker));
+            if (err == 0xFFFFFFFFu && (pl <= 0.0 || pr <= 0.0)) err = ((key + 1) << 12) | (2u << 10) | (uint32_t)cl_;
+            const double vnl = dvd(ql[1 + axis], rl);
+            const double vnr = dvd(qr[1 + axis], rr);
+            const double sa = add(fabs(vnl), dsqrt(dvd(mul(gamma, pl), rl)));
+            const double sb = add(fabs(vnr), dsqrt(dvd(mul(gamma, pr), rr)));
+            const double s = sb > sa ? sb : sa;  // Python max(sa, sb)
+            if (s > smax) smax = s;
+            const double hs = mul(0.5, s);
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) {
+                const double ul = ql[v], ur = qr[v];
+                double flv, frv;
+                if (v == 0) {
+                    flv = mul(rl, vnl);
+                    frv = mul(rr, vnr);
+                } else if (v == 4) {
+                    flv = mul(add(ul, pl), vnl);
+                    frv = mul(add(ur, pr), vnr);
+                } else {
+                    flv = mul(ul, vnl);
+                    frv = mul(ur, vnr);
+                    if (v == 1 + axis) {
+                        flv = add(flv, pl);
+                        frv = add(frv, pr);
+                    }
+                }
+                acc[v] = add(acc[v], mul(w, sub(mul(0.5, add(flv, frv)), mul(hs, sub(ur, ul)))));
+            }
+        }
+        double* F;
+        if (axis == 0) F = FX + b * 5 * 576 + (i * 8 + j) * 9 + k;
+        else if (axis == 1) F = FY + b * 5 * 576 + (i * 9 + j) * 8 + k;
+        else F = FZ + b * 5 * 576 + (j * 8 + i) * 8 + k;
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) F[v * 576] = acc[v];
+    }
+    atomicMax(&s_smax, (unsigned long long)__double_as_longlong(smax));
+    if (err != 0xFFFFFFFFu) atomicMin(&s_err, err);
+    __syncthreads();
+    if (t == 0) {
+        smax_out[b] = __longlong_as_double((long long)s_smax);
+        err_out[b] = s_err;
+        if (latch && s_err != 0xFFFFFFFFu) atomicMin(latch + b, s_err);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // fused reconstruct + flux (batched step path): U block and per-cell
 // {uc, minmod slopes} in shared memory, every quadrature state rebuilt on the
 // fly with the reconstruct_kernel expression tree -- Q (1.04 MB/subgrid) is
@@ -573,6 +681,16 @@ int sg_flux(const double* Q, int64_t nleaves, double gamma, double* FX, double* 
     if (nleaves <= 0) return SG_OK;
     flux_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax, err, latch);
     return sg_check_launch("sg_flux");
+}
+
+int sg_flux_legacy(const double* Q, int64_t nleaves, double gamma, double* FX, double* FY, double* FZ,
+                   double* smax, uint32_t* err, uint32_t* latch, void* stream) {
+    int rc = init_tables();
+    if (rc) return rc;
+    if (nleaves <= 0) return SG_OK;
+    flux_legacy_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax,
+                                                                                      err, latch);
+    return sg_check_launch("sg_flux_legacy");
 }
 
 int sg_hydro_fused(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,

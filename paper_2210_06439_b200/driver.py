@@ -39,7 +39,7 @@ STAR_K = 1.0
 STAR_ATMOSPHERE = 0.05
 
 KERNEL_ORDER = ("reconstruct", "flux", "hydro_update", "monopole", "multipole")
-HYDRO_KERNELS = ("cuda", "simd", "scalar")    # all three run the same bit-exact CUDA kernels
+HYDRO_KERNELS = ("cuda", "simd", "scalar", "legacy")  # the first three run the same bit-exact kernels
 GRAVITY_KERNELS = ("cuda", "simd", "scalar")
 WARP_WIDTH = 32
 
@@ -183,16 +183,15 @@ def run_scenario(cfg: ScenarioConfig, backend: str = "scalar", threads: int = 1,
     if tasks_per_multipole < 1:
         raise ValueError(f"tasks_per_multipole must be >= 1, got {tasks_per_multipole}")
     if hydro_kernel not in HYDRO_KERNELS:
-        raise ValueError(f"hydro_kernel must be one of {HYDRO_KERNELS}, got {hydro_kernel!r}"
-                         + (" (the legacy straight-line kernels are not ported)" if hydro_kernel == "legacy"
-                            else ""))
+        raise ValueError(f"hydro_kernel must be one of {HYDRO_KERNELS}, got {hydro_kernel!r}")
     if gravity_kernel not in GRAVITY_KERNELS:
         raise ValueError(f"gravity_kernel must be one of {GRAVITY_KERNELS}, got {gravity_kernel!r}")
 
     tree = init_scenario(cfg)
     # per-kernel records in the reference's per-leaf semantics: the unfused
     # reconstruct -> flux pair keeps "reconstruct" and "flux" separate
-    st = UnigridState(cfg.max_level, cfg.hydro, cfg.gravity, fused_hydro=False)
+    st = UnigridState(cfg.max_level, cfg.hydro, cfg.gravity, fused_hydro=False,
+                      legacy_flux=hydro_kernel == "legacy")
     st.load({name: global_field(tree, name) for name in HYDRO_FIELDS})
     st.timers = {}
     launches0 = _lib.LAUNCHES["count"]

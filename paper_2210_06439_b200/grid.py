@@ -36,7 +36,8 @@ class UnigridState:
     """One rank's z-slab of a periodic level-L unigrid, resident on a GPU."""
 
     def __init__(self, level: int, hydro: HydroConfig | None = None, gravity: GravityConfig | None = None,
-                 slab: Slab | None = None, device=None, group=None, fused_hydro: bool = True):
+                 slab: Slab | None = None, device=None, group=None, fused_hydro: bool = True,
+                 legacy_flux: bool = False):
         B.require_device()
         self.level = level
         self.slab = slab or Slab(level)
@@ -66,7 +67,8 @@ class UnigridState:
         nb = self.nleaves
         # fused reconstruct+flux never materialises Q; the unfused (drop-in
         # kernel pair) path allocates it lazily
-        self.fused_hydro = fused_hydro
+        self.fused_hydro = fused_hydro and not legacy_flux
+        self.legacy_flux = legacy_flux   # reference kernels/legacy.py flux formulation
         self._Q = None
         self.FX = torch.empty((nb, 5, 8, 8, 9), **f64)
         self.FY = torch.empty((nb, 5, 8, 9, 8), **f64)
@@ -230,8 +232,9 @@ class UnigridState:
             B.reconstruct(self.U, self.uv, self.leaves, self.nleaves, self.h.positivity_floor, self.Q)
             self._done(ev)
             ev = self._t("flux")
-            B.flux(self.Q, self.nleaves, self.h.gamma, self.FX, self.FY, self.FZ, self.smax, self.flux_err,
-                   self.flux_latch)
+            fl = B.flux_legacy if self.legacy_flux else B.flux
+            fl(self.Q, self.nleaves, self.h.gamma, self.FX, self.FY, self.FZ, self.smax, self.flux_err,
+               self.flux_latch)
             self._done(ev)
         ev = self._t("hydro_update")
         B.hydro_update(self.U, self.uv, self.leaves, self.nleaves, self.FX, self.FY, self.FZ, self.smax,

@@ -385,6 +385,64 @@ def scenario_runs(man):
     man["scenarios"] = rec
 
 
+def legacy(man):
+    """Reference legacy straight-line kernels (kernels/legacy.py): per random
+    block Q and fluxes, error cases, and whole legacy-hydro scenario runs."""
+    from simdgrid.driver import run_scenario
+    from simdgrid.kernels import legacy as LG
+    from simdgrid.octree import SubGrid
+    from simdgrid.scenarios import ScenarioConfig
+    g = np.load(HERE / "hydro_random.npz")
+    out = {}
+    h = K.HydroConfig()
+    for i in range(6):
+        sub = SubGrid.allocate(0, (0, 0, 0), 1.0 / 64)
+        for v, name in enumerate(FIELDS):
+            sub.fields[name][...] = g[f"U{i}"][v]
+        q = LG.legacy_reconstruct(sub, h)
+        out[f"Qdigest{i}"] = np.array(digest(q.values))
+        try:
+            fl = LG.legacy_flux(sub, q, h)
+            out[f"FX{i}"], out[f"FY{i}"], out[f"FZ{i}"] = fl.fx, fl.fy, fl.fz
+            out[f"smax{i}"] = np.array(fl.max_speed)
+        except K.KernelError as exc:
+            out[f"err{i}"] = np.array(str(exc))
+    # kernel-level error codes (first error, left cell) on block 0's Q
+    from simdgrid.kernels.geometry import DIR_MINUS, DIR_PLUS, DIRECTIONS_F, SIMPSON_W
+    Q = np.empty((5, 26, 10, 10, 10))
+    compiled.reconstruct_kernel(np.ascontiguousarray(g["U0"]), 1e-12, 1, DIRECTIONS_F, Q)
+    errs = []
+    for case in range(4):
+        Qe = Q.copy()
+        if case == 0:
+            Qe[0, :, 4, 4, 4] = -1.0
+        elif case == 1:
+            Qe[4, :, 4, 4, 4] = 1e-9
+            Qe[1, :, 4, 4, 4] = 1.0
+        elif case == 2:
+            Qe[0, :, 7, 7, 7] = 0.0
+            Qe[4, :, 2, 3, 4] = 1e-12
+            Qe[1, :, 2, 3, 4] = 5.0
+        else:
+            Qe[0, :, 5, 5, 5] = np.nan
+        FX, FY, FZ = np.empty((5, 8, 8, 9)), np.empty((5, 8, 9, 8)), np.empty((5, 9, 8, 8))
+        smax, code, cell = LG._legacy_flux_impl(Qe, 1.4, DIR_PLUS, DIR_MINUS, SIMPSON_W, FX, FY, FZ)
+        errs.append([smax, code, cell])
+        out[f"errFX{case}"] = FX
+    out["flux_errors"] = np.array(errs)
+    np.savez_compressed(HERE / "legacy.npz", **out)
+    names = ("rho", "sx", "sy", "sz", "E", "phi", "gx", "gy", "gz")
+    rec = {}
+    for name, level, steps in (("blast", 1, 2), ("rotating-star-proxy", 1, 1)):
+        cfg = ScenarioConfig(name, max_level=level, stop_step=steps)
+        res = run_scenario(cfg, backend="scalar", threads=os.cpu_count() or 4, hydro_kernel="legacy")
+        rec[f"{name}_L{level}_s{steps}"] = {
+            "level": level, "steps": steps,
+            "field_digests": {n: digest(global_from_tree(res.tree, n)) for n in names},
+        }
+    man["legacy_scenarios"] = rec
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-l4", action="store_true")
@@ -393,7 +451,7 @@ def main():
     man_path = HERE / "manifest.json"
     man = json.loads(man_path.read_text()) if man_path.exists() else {}
     todo = args.only.split(",") if args.only else [
-        "cfg1", "tree", "hydro_random", "cfg2", "cfg4", "cfg3", "cfg5_L2", "cfg5_L4", "scenarios"]
+        "cfg1", "tree", "hydro_random", "cfg2", "cfg4", "cfg3", "cfg5_L2", "cfg5_L4", "scenarios", "legacy"]
     for name in todo:
         if name == "cfg5_L4" and args.skip_l4:
             continue
@@ -403,7 +461,7 @@ def main():
          "hydro_random": lambda: hydro_random(), "cfg2": lambda: cfg2_p2p(man),
          "cfg3": lambda: cfg3_m2l(man), "cfg4": lambda: cfg4_hydro(man),
          "cfg5_L2": lambda: cfg5(man, 2, "every"), "cfg5_L4": lambda: cfg5(man, 4, "last"),
-         "scenarios": lambda: scenario_runs(man)}[name]()
+         "scenarios": lambda: scenario_runs(man), "legacy": lambda: legacy(man)}[name]()
         man["_generator"] = "tests/golden/make_golden.py (reference simdgrid, numba compiled path)"
         man_path.write_text(json.dumps(man, indent=1, sort_keys=True))
         print(f"[golden] {name} done in {time.time() - t0:.1f}s", flush=True)

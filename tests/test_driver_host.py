@@ -104,7 +104,5 @@ class TestCsv:
             D.run_scenario(cfg, tasks_per_multipole=0)
         with pytest.raises(ValueError, match="hydro_kernel"):
             D.run_scenario(cfg, hydro_kernel="turbo")
-        with pytest.raises(ValueError, match="legacy"):
-            D.run_scenario(cfg, hydro_kernel="legacy")
         with pytest.raises(ValueError):
             D.sweep(cfg, [], ["scalar"], "x.csv")
