@@ -294,23 +294,34 @@ def run_ours(args) -> None:
     total_leaves = 8 ** LEVEL
     value = total_leaves * args.steps / elapsed
 
-    # e2e through the public host API (pinned host buffers, copies timed)
-    host_in = {k: torch.from_numpy(np.ascontiguousarray(state[k][slab.z0:slab.z0 + slab.nz])).pin_memory()
-               for k in ("rho", "sx", "sy", "sz", "E")}
-    p = grid.U_PAD
-    host_out = torch.empty((9, slab.nz, slab.n, slab.n), dtype=torch.float64).pin_memory()
+    # e2e through the public host API (grid.HostPipeline): every step uploads
+    # its input state from pinned host memory and reads the new state and
+    # gravity back into pinned host memory; transfers overlap compute on a
+    # copy stream (double-buffered staging); timed until the last readback
+    host_in = torch.from_numpy(np.ascontiguousarray(
+        np.stack([state[k][slab.z0:slab.z0 + slab.nz] for k in ("rho", "sx", "sy", "sz", "E")]))).pin_memory()
+    host_out = [torch.empty((9, slab.nz, slab.n, slab.n), dtype=torch.float64).pin_memory() for _ in range(2)]
+    pipe = grid.HostPipeline(u)
     e2e_steps = max(1, args.steps)
+    for j in range(2):  # warm the pipeline (streams, events, staging)
+        pipe.submit(host_in, host_out[j % 2])
+    pipe.synchronize()
     barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        for v, k in enumerate(("rho", "sx", "sy", "sz", "E")):
-            u.U[v, p:p + slab.nz, p:p + slab.n, p:p + slab.n].copy_(host_in[k], non_blocking=True)
-        u.step()
-        host_out[:5].copy_(u.U[:, p:p + slab.nz, p:p + slab.n, p:p + slab.n], non_blocking=True)
-        host_out[5:].copy_(u.grav, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+    for j in range(e2e_steps):
+        pipe.submit(host_in, host_out[j % 2])
+    pipe.synchronize()
     barrier()
     e2e_s = time.perf_counter() - t0
+    u.check_errors()
+    ref_out = grid.UnigridState(LEVEL, HydroConfig(gamma=1.4), GravityConfig(theta=0.34, eps=0.5, expansion_order=1),
+                                slab=slab, group=group) if args.verify_e2e else None
+    if ref_out is not None:  # the pipelined result equals load + step + fetch
+        ref_out.load(state)
+        ref_out.step()
+        f = ref_out.fetch()
+        want = np.stack([f[k] for k in ("rho", "sx", "sy", "sz", "E", "phi", "gx", "gy", "gz")])
+        assert np.array_equal(host_out[(e2e_steps - 1) % 2].numpy(), want), "pipelined e2e result differs"
     t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -373,6 +384,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--verify-e2e", action="store_true", help="check the pipelined e2e result bitwise")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -283,6 +283,63 @@ class UnigridState:
                           f"(x={detail % 8}, y={(detail // 8) % 8}, z={detail // 64}) of leaf {coord}")
 
 
+class HostPipeline:
+    """Host-buffer stepping with copy/compute overlap: each ``submit`` takes a
+    pinned host state (5, nz, n, n), runs one timestep on it and returns the
+    new state plus gravity (9, nz, n, n) into a pinned host buffer.  Uploads
+    and readbacks run on copy streams through double-buffered device
+    staging, so submission k's transfers overlap the compute of k-1 / k+1
+    (independent inputs, e.g. ensembles or a stream of snapshots).  Results
+    are those of ``UnigridState.load`` + ``step`` + ``fetch``."""
+
+    def __init__(self, state: UnigridState):
+        self.st = state
+        dev = state.device
+        shp = (5, state.nz, state.n, state.n)
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.u_in = [torch.empty(shp, **f64) for _ in range(2)]
+        self.out = [torch.empty((9,) + shp[1:], **f64) for _ in range(2)]
+        # separate upload and download streams: on one FIFO stream upload k+1
+        # would queue behind readback k, which waits for step k to finish
+        self.up = torch.cuda.Stream(device=dev)
+        self.down = torch.cuda.Stream(device=dev)
+        self.ev_h2d = [torch.cuda.Event() for _ in range(2)]
+        self.ev_in_free = [torch.cuda.Event() for _ in range(2)]
+        self.ev_result = [torch.cuda.Event() for _ in range(2)]
+        self.ev_out_free = [torch.cuda.Event() for _ in range(2)]
+        for e in self.ev_in_free + self.ev_out_free:
+            e.record()
+        self.k = 0
+
+    def submit(self, host_in: torch.Tensor, host_out: torch.Tensor, **step_kw) -> torch.cuda.Event:
+        st, i = self.st, self.k % 2
+        p, nz, n = U_PAD, st.nz, st.n
+        comp = torch.cuda.current_stream(st.device)
+        with torch.cuda.stream(self.up):
+            self.up.wait_event(self.ev_in_free[i])
+            self.u_in[i].copy_(host_in, non_blocking=True)
+            self.ev_h2d[i].record(self.up)
+        comp.wait_event(self.ev_h2d[i])
+        st.U[:, p:p + nz, p:p + n, p:p + n].copy_(self.u_in[i])
+        self.ev_in_free[i].record(comp)
+        st.step(**step_kw)
+        comp.wait_event(self.ev_out_free[i])
+        self.out[i][:5].copy_(st.U[:, p:p + nz, p:p + n, p:p + n])
+        self.out[i][5:].copy_(st.grav)
+        self.ev_result[i].record(comp)
+        with torch.cuda.stream(self.down):
+            self.down.wait_event(self.ev_result[i])
+            host_out.copy_(self.out[i], non_blocking=True)
+            self.ev_out_free[i].record(self.down)
+        self.k += 1
+        return self.ev_out_free[i]
+
+    def synchronize(self) -> None:
+        self.up.synchronize()
+        self.down.synchronize()
+        torch.cuda.current_stream(self.st.device).synchronize()
+
+
 class LocalSlabs:
     """The z-slab decomposition with all P slabs in one process on one
     device: same kernels, same halo planes as the NCCL path, exchanged by
