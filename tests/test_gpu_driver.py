@@ -82,3 +82,49 @@ def test_cuda_profiler_and_device_source_cubes():
     st.to_tree(tree)
     assert not np.array_equal(tree.leaves[0].interior("phi"), before["phi"])  # gravity written back
     assert torch.cuda.is_available()
+
+
+def test_c4_blast_conservation_and_48_symmetry():
+    """reference tests/test_acceptance.py:282-318 on the GPU harness: blast at
+    L=2 for 10 steps conserves mass/energy/momentum to 1e-12 and the final
+    density is invariant under the 48 cube symmetries to 1e-12."""
+    import itertools
+
+    import numpy as np
+    cfg = D.ScenarioConfig("blast", max_level=2, stop_step=10)
+    result = D.run_scenario(cfg, backend="emulated8", threads=2)
+    init = D.init_scenario(cfg)
+    dx3 = result.tree.dx ** 3
+
+    def totals(tree):
+        return {n: float(sum(leaf.interior(n).sum() for leaf in tree.leaves)) * dx3
+                for n in ("rho", "sx", "sy", "sz", "E")}
+
+    before, after = totals(init), totals(result.tree)
+    assert abs(after["rho"] - before["rho"]) / abs(before["rho"]) <= 1e-12
+    assert abs(after["E"] - before["E"]) / abs(before["E"]) <= 1e-12
+    for n in ("sx", "sy", "sz"):
+        scale = float(sum(np.abs(leaf.interior(n)).sum() for leaf in result.tree.leaves)) * dx3
+        assert abs(after[n] - before[n]) / max(scale, 1e-300) <= 1e-12
+    rho = global_field(result.tree, "rho")
+    worst = 0.0
+    for perm in itertools.permutations(range(3)):
+        for flips in itertools.product((False, True), repeat=3):
+            g = np.transpose(rho, perm)
+            for ax, f in enumerate(flips):
+                if f:
+                    g = np.flip(g, axis=ax)
+            worst = max(worst, float(np.max(np.abs(g - rho))))
+    assert worst / float(np.max(np.abs(rho))) <= 1e-12
+
+
+def test_c5_backend_and_task_invariance():
+    """reference test_acceptance.py:321-356: backend / threads / tasks never
+    change the bits."""
+    cfg = D.ScenarioConfig("rotating-star-proxy", max_level=2, stop_step=1)
+    ref = None
+    for backend, threads, tpm in (("scalar", 1, 1), ("emulated8", 4, 16), ("emulated2", 2, 7)):
+        res = D.run_scenario(cfg, backend=backend, threads=threads, tasks_per_multipole=tpm)
+        fb = b"".join(leaf.interior(n).tobytes() for leaf in res.tree.leaves for n in NAMES)
+        ref = fb if ref is None else ref
+        assert fb == ref
