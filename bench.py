@@ -48,7 +48,7 @@ METRIC = "FP64 subgrids/s per kernel (M2L, P2P, hydro) at 1/2/4/8 B200; % FP64/H
 UNIT = "subgrids/s"
 M2L_FLOP = {1: 26_800_128, 0: 8_338_944}      # SURVEY.md §8(d), per subgrid
 P2P_FLOP = 423_936
-HYDRO_ITER_FLOP = 1_174_000 + 1_275_264 + 17_920   # reconstruct + flux + update
+HYDRO_ITER_FLOP = 1_174_000 + 1_275_264         # reconstruct + flux
 LEVEL = 4
 
 
@@ -234,6 +234,84 @@ def fp64_peak(torch) -> dict:
     return res
 
 
+def per_config_rates(torch, peaks: dict) -> dict:
+    """Per-kernel device rates on BASELINE configs 1-4 (SURVEY.md 8(d)
+    restatements), median of 5 CUDA-event timed launches after a warm-up;
+    inputs resident.  FP64 fractions are against the measured DADD issue peak
+    (the attainable roof without FMA contraction); reconstruct's against HBM."""
+    import statistics as stats
+
+    from paper_2210_06439_b200 import batched as B
+    from paper_2210_06439_b200 import grid, scenarios
+    from paper_2210_06439_b200.batched import View
+    from paper_2210_06439_b200.kernels import GravityConfig, HydroConfig
+
+    def timed(fn, reps=5):
+        fn()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        return stats.median(ts)
+
+    issue = peaks["dadd_tflops"] * 1e12
+    hbm = None
+    try:
+        hbm = json.loads((REPO / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] * 1e9
+    except Exception:
+        pass
+    out = {}
+    g1 = GravityConfig(theta=0.34, eps=0.5, expansion_order=1)
+    # config 1: one 24^3 neighbourhood (latency: one CTA)
+    cube = torch.from_numpy(scenarios.config1_cube(0)).cuda()
+    cl = torch.empty((12, 12, 12, 4), dtype=torch.float64, device="cuda")
+    res = torch.empty((4, 8, 8, 8), dtype=torch.float64, device="cuda")
+    dx = 1.0 / 64
+    rad = dx / 0.34
+    eps = 0.5 * dx
+
+    def c1():
+        B.cluster_aggregate(cube, dx, cl)
+        B.m2l(cube, View(8, 8, 8, 8), cl, 0, None, 1, dx, rad * rad, eps * eps, 1, res, View(8, 8, 8, 0))
+    t = timed(c1)
+    out["config1_m2l_single"] = {"latency_us": t * 1e6, "subgrids_per_s": 1 / t}
+    # configs 2-4 on the 512-subgrid level-3 grid
+    u = grid.UnigridState(3, HydroConfig(gamma=5.0 / 3.0), g1)
+    z = np.zeros((64, 64, 64))
+    for name, rho in (("config2_p2p", scenarios.config2_rho(1, 3)), ("config3_m2l", scenarios.config3_rho(3))):
+        u.load({"rho": rho, "sx": z, "sy": z, "sz": z, "E": rho})
+        u.set_mass()
+        u._halo(u.mass, 1, u.mv)
+        B.cluster_aggregate(u.mass, u.dx, u.clusters)
+        if name == "config2_p2p":
+            t = timed(lambda: B.p2p(u.mass, u.mv, u.leaves, u.nleaves, u.dx, u.rad2, u.eps2, u.halo, u.grav, u.gv))
+            flop = P2P_FLOP
+        else:
+            t = timed(lambda: B.m2l(u.mass, u.mv, u.clusters, 0, u.leaves, u.nleaves, u.dx, u.rad2, u.eps2, 1,
+                                    u.grav, u.gv))
+            flop = M2L_FLOP[1]
+        out[name] = {"ms": t * 1e3, "subgrids_per_s": 512 / t, "tflops": flop * 512 / t / 1e12,
+                     "frac_fp64_issue": flop * 512 / t / issue}
+    u.load(scenarios.config4_state(3))
+    u._halo(u.U, 5, u.uv)
+    tf = timed(lambda: B.hydro_fused(u.U, u.uv, u.leaves, u.nleaves, 1e-12, 5.0 / 3.0, u.FX, u.FY, u.FZ, u.smax,
+                                     u.flux_err))
+    tr = timed(lambda: B.reconstruct(u.U, u.uv, u.leaves, u.nleaves, 1e-12, u.Q))
+    tx = timed(lambda: B.flux(u.Q, u.nleaves, 5.0 / 3.0, u.FX, u.FY, u.FZ, u.smax, u.flux_err))
+    rec = {"fused_ms": tf * 1e3, "subgrids_per_s": 512 / tf,
+           "fused_frac_fp64_issue": HYDRO_ITER_FLOP * 512 / tf / issue,
+           "reconstruct_ms": tr * 1e3, "flux_ms": tx * 1e3, "unfused_subgrids_per_s": 512 / (tr + tx)}
+    if hbm:
+        rec["reconstruct_frac_hbm"] = 1_109_120 * 512 / tr / hbm
+        rec["flux_frac_hbm"] = 1_109_128 * 512 / tx / hbm
+    out["config4_hydro"] = rec
+    return out
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -360,6 +438,10 @@ def run_ours(args) -> None:
     }
     if rank == 0:
         line["clocks"] = clk.summary()
+        try:
+            line["per_config"] = per_config_rates(torch, peaks)
+        except Exception as exc:  # informational; never fails the headline
+            line["per_config"] = {"error": str(exc)}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             from oracle import oracle as O

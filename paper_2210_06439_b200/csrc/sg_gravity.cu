@@ -360,6 +360,12 @@ template <int ORDER, bool SMALL_NEAR>
 __global__ void __launch_bounds__(M2L_THREADS, 1)
 m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int64_t B, double dx,
            double rad2, double eps2, int i0, int i1, FieldView ov, double* __restrict__ work) {
+    // blockDim.x = targets per CTA (512, or fewer for small batches: a leaf's
+    // 512 targets are then split over 512/blockDim.x CTAs so more SMs work)
+    const int nt = blockDim.x;
+    const int chunks = M2L_THREADS / nt;
+    const int chunk = blockIdx.x % chunks;
+    const int64_t g0 = blockIdx.x / chunks, G = gridDim.x / chunks;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* tab = reinterpret_cast<double*>(smem_raw);
     double2* near_tab = reinterpret_cast<double2*>(tab + TAB_N * TAB_N * TAB_PITCH);
@@ -371,7 +377,7 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
     double* wk = work + (int64_t)blockIdx.x * (27 * 4 * M2L_THREADS) + tid;
 
     // -- far geometry table, keyed by (|kx|,|ky|,|kz|) - 1/2 (compiled.py:394-414)
-    for (int e = tid; e < TAB_N * TAB_N * TAB_N; e += M2L_THREADS) {
+    for (int e = tid; e < TAB_N * TAB_N * TAB_N; e += nt) {
         const int ax = e % TAB_N, ay = (e / TAB_N) % TAB_N, az = e / (TAB_N * TAB_N);
         // |t - (b + 1)| = a + 1/2 exactly; RN is sign-symmetric so |r| = (a+1/2)*dx
         const double rx = mul(add((double)ax, 0.5), dx);
@@ -392,15 +398,15 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
         }
     }
     // -- near-cell table keyed by integer |s| per axis (compiled.py:429-438)
-    if (tid < NEAR_R * NEAR_R * NEAR_R) {
-        const int ix = tid % NEAR_R, iy = (tid / NEAR_R) % NEAR_R, iz = tid / (NEAR_R * NEAR_R);
+    for (int e = tid; e < NEAR_R * NEAR_R * NEAR_R; e += nt) {
+        const int ix = e % NEAR_R, iy = (e / NEAR_R) % NEAR_R, iz = e / (NEAR_R * NEAR_R);
         const double sx = mul((double)ix, dx), sy = mul((double)iy, dx), sz = mul((double)iz, dx);
         const double r2s = add(add(mul(sx, sx), mul(sy, sy)), mul(sz, sz));
         if (r2s > 0.0) {
             const double invs = dvd(1.0, dsqrt(add(r2s, eps2)));
-            near_tab[tid] = make_double2(invs, mul(mul(invs, invs), invs));
+            near_tab[e] = make_double2(invs, mul(mul(invs, invs), invs));
         } else {
-            near_tab[tid] = make_double2(-1.0, 0.0);
+            near_tab[e] = make_double2(-1.0, 0.0);
         }
     }
 
@@ -414,8 +420,8 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
         }
     }
 
-    const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;
-    const int f = (z * 8 + y) * 8 + x;
+    const int f = chunk * nt + tid;  // this thread's target, flat [z][y][x]
+    const int x = f & 7, y = (f >> 3) & 7, z = f >> 6;
     const bool active = f >= i0 && f < i1;
     const double tx = (double)x + 0.5, ty = (double)y + 0.5, tz = (double)z + 0.5;
     double rxv[NC];
@@ -427,7 +433,7 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
         axv[c] = fold(x - 2 * c + 7);
     }
 
-    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    for (int64_t b = g0; b < B; b += G) {
         __syncthreads();
         {  // stage this leaf's 12^3 clusters
             int64_t cx0 = cv.off, cy0 = cv.off, cz0 = cv.off;
@@ -437,7 +443,7 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
                 cz0 += 4 * (int64_t)leaves[3 * b + 2];
             }
             const double4* src = cv.base + b * cv.leaf_stride + cz0 * cv.sz + cy0 * cv.sy + cx0;
-            for (int i = tid; i < NC * NC * NC; i += M2L_THREADS) {
+            for (int i = tid; i < NC * NC * NC; i += nt) {
                 const int cx = i % NC, cy = (i / NC) % NC, cz = i / (NC * NC);
                 const double2* s2 = reinterpret_cast<const double2*>(src + cz * cv.sz + cy * cv.sy + cx);
                 const double2 a = __ldg(s2), c2 = __ldg(s2 + 1);
@@ -446,7 +452,7 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
         }
         const double* mc = leaf_origin(mv, leaves, b, 8);
         if (SMALL_NEAR) {  // stage the near-field masses
-            for (int i = tid; i < NBW * NBW * NBW; i += M2L_THREADS) {
+            for (int i = tid; i < NBW * NBW * NBW; i += nt) {
                 const int cx = i % NBW, cy = (i / NBW) % NBW, cz = i / (NBW * NBW);
                 nm[i] = __ldg(mc + (int64_t)(cz + NB0) * mv.sz + (int64_t)(cy + NB0) * mv.sy + (cx + NB0));
             }
@@ -629,9 +635,27 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     return sg_check_launch("sg_p2p");
 }
 
+// launch shape: one 512-thread CTA per SM over the leaves, or -- for batches
+// smaller than the SM count -- each leaf's targets split over up to 16 CTAs
+// (down to one warp each) so the single-subgrid case uses 16 SMs, not 1
+static void m2l_shape(int64_t nleaves, int* threads, int64_t* grid) {
+    const int64_t sms = sm_count();
+    if (nleaves >= sms) {
+        *threads = M2L_THREADS;
+        *grid = sms;
+        return;
+    }
+    int chunks = 1;
+    while (chunks < 16 && nleaves * chunks * 2 <= sms) chunks *= 2;
+    *threads = M2L_THREADS / chunks;
+    *grid = nleaves * chunks;
+}
+
 int64_t sg_m2l_workspace_bytes(int64_t nleaves) {
-    const int64_t grid = nleaves < sm_count() ? nleaves : sm_count();
-    return (grid > 0 ? grid : 1) * M2L_WORK_PER_CTA * (int64_t)sizeof(double);
+    int threads;
+    int64_t grid;
+    m2l_shape(nleaves > 0 ? nleaves : 1, &threads, &grid);
+    return grid * M2L_WORK_PER_CTA * (int64_t)sizeof(double);
 }
 
 int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
@@ -661,13 +685,15 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     cv.leaf_stride = cluster_leaf_stride / 4;
     cv.off = (pad - 8) / 2;
     FieldView ov = make_view(out, onx, ony, onz, 0, out_leaf_stride);
-    const int64_t grid = nleaves < sm_count() ? nleaves : sm_count();
+    int threads;
+    int64_t grid;
+    m2l_shape(nleaves, &threads, &grid);
     // every near cluster within |k| <= 5/2 per axis (conservative margin)
     const bool small_near = rad2 < 12.5 * dx * dx;
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M2L_SMEM);
-        kern<<<(unsigned)grid, M2L_THREADS, M2L_SMEM, (cudaStream_t)stream>>>(mv, cv, leaves, nleaves, dx, rad2,
-                                                                             eps2, i0, i1, ov, workspace);
+        kern<<<(unsigned)grid, threads, M2L_SMEM, (cudaStream_t)stream>>>(mv, cv, leaves, nleaves, dx, rad2, eps2,
+                                                                         i0, i1, ov, workspace);
     };
     if (order == 1) {
         if (small_near) launch(m2l_kernel<1, true>);
