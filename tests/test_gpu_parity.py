@@ -379,3 +379,52 @@ def test_host_pipeline_equals_load_step_fetch():
         f = ref.fetch()
         want = np.stack([f[k] for k in octree.HYDRO_FIELDS + ("phi", "gx", "gy", "gz")])
         assert bitwise(hout.numpy(), want)
+
+
+def test_batched_kernels_on_permuted_leaf_subsets(manifest):
+    """The leaf list is arbitrary: a random subset in random order (so CTAs
+    see scattered coordinates, and the small-batch M2L split path runs) gives
+    every leaf exactly its golden bits."""
+    rng = np.random.default_rng(123)
+    n, level = 64, 3
+    rho = scenarios.config3_rho(level)
+    m = manifest["cfg3_m2l"]
+    if digest(rho) != m["input_digest"]:
+        pytest.skip("config-3 generator differs on this host")
+    mv = View(n, n, n, 8)
+    mass = torch.zeros(mv.padded_shape, dtype=torch.float64, device="cuda")
+    mass[8:8 + n, 8:8 + n, 8:8 + n] = dev(rho * (1.0 / 64) ** 3)
+    B.fill_periodic(mass, 1, mv, 7)
+    z_, y_, x_ = mv.padded_shape
+    cl = torch.empty((z_ // 2, y_ // 2, x_ // 2, 4), dtype=torch.float64, device="cuda")
+    B.cluster_aggregate(mass, 1.0 / 64, cl)
+    rad2, eps2 = K.gravity_params(1.0 / 64, K.GravityConfig())
+    allc = [(x, y, z) for z in range(8) for y in range(8) for x in range(8)]
+    for count in (3, 40, 200):
+        pick = [allc[i] for i in rng.permutation(512)[:count]]
+        leaves = torch.tensor(pick, dtype=torch.int32, device="cuda")
+        out = torch.zeros((4, n, n, n), dtype=torch.float64, device="cuda")
+        B.m2l(mass, mv, cl, 0, leaves, count, 1.0 / 64, rad2, eps2, 1, out, View(n, n, n, 0))
+        o = out.cpu().numpy()
+        for (cx, cy, cz) in pick:
+            blk = o[:, cz * 8:cz * 8 + 8, cy * 8:cy * 8 + 8, cx * 8:cx * 8 + 8]
+            assert digest(blk) == m["o1"]["leaf_digests"]["%d,%d,%d" % (cx, cy, cz)], (count, cx, cy, cz)
+    # hydro: fused kernel on a permuted subset vs the config-4 per-leaf golden
+    m4 = manifest["cfg4_hydro"]
+    gamma = float.fromhex(m4["gamma"])
+    u = G.UnigridState(3, K.HydroConfig(gamma=gamma))
+    u.load(scenarios.config4_state(3))
+    u._halo(u.U, 5, u.uv)
+    pick = [allc[i] for i in rng.permutation(512)[:77]]
+    leaves = torch.tensor(pick, dtype=torch.int32, device="cuda")
+    FX = torch.empty((77, 5, 8, 8, 9), dtype=torch.float64, device="cuda")
+    FY = torch.empty((77, 5, 8, 9, 8), dtype=torch.float64, device="cuda")
+    FZ = torch.empty((77, 5, 9, 8, 8), dtype=torch.float64, device="cuda")
+    smax = torch.empty(77, dtype=torch.float64, device="cuda")
+    err = torch.empty(77, dtype=torch.int32, device="cuda")
+    B.hydro_fused(u.U, u.uv, leaves, 77, 1e-12, gamma, FX, FY, FZ, smax, err)
+    FXh, FZh, sm = FX.cpu().numpy(), FZ.cpu().numpy(), smax.cpu().numpy()
+    for b, (cx, cy, cz) in enumerate(pick):
+        rec = m4["leaves"]["%d,%d,%d" % (cx, cy, cz)]
+        assert digest(FXh[b]) == rec["fx"] and digest(FZh[b]) == rec["fz"]
+        assert sm[b] == float.fromhex(rec["smax"])
