@@ -655,6 +655,8 @@ int64_t sg_m2l_workspace_bytes(int64_t nleaves) {
     int threads;
     int64_t grid;
     m2l_shape(nleaves > 0 ? nleaves : 1, &threads, &grid);
+    const int64_t sms = sm_count();
+    if (grid < sms && nleaves > sms) grid = sms;
     return grid * M2L_WORK_PER_CTA * (int64_t)sizeof(double);
 }
 
@@ -685,22 +687,48 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     cv.leaf_stride = cluster_leaf_stride / 4;
     cv.off = (pad - 8) / 2;
     FieldView ov = make_view(out, onx, ony, onz, 0, out_leaf_stride);
-    int threads;
-    int64_t grid;
-    m2l_shape(nleaves, &threads, &grid);
     // every near cluster within |k| <= 5/2 per axis (conservative margin)
     const bool small_near = rad2 < 12.5 * dx * dx;
-    auto launch = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M2L_SMEM);
-        kern<<<(unsigned)grid, threads, M2L_SMEM, (cudaStream_t)stream>>>(mv, cv, leaves, nleaves, dx, rad2, eps2,
-                                                                         i0, i1, ov, workspace);
+    // launch [first, first+count) of the leaf list with its own shape
+    auto launch_range = [&](int64_t first, int64_t count) {
+        int threads;
+        int64_t grid;
+        m2l_shape(count, &threads, &grid);
+        FieldView mvr = mv, ovr = ov;
+        ClusterView cvr = cv;
+        const int32_t* lv = leaves;
+        if (leaves) {
+            lv = leaves + 3 * first;
+        } else {
+            mvr.base += first * mv.leaf_stride;
+            ovr.base += first * ov.leaf_stride;
+            cvr.base += first * cv.leaf_stride;
+        }
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M2L_SMEM);
+            kern<<<(unsigned)grid, threads, M2L_SMEM, (cudaStream_t)stream>>>(mvr, cvr, lv, count, dx, rad2, eps2,
+                                                                             i0, i1, ovr, workspace);
+        };
+        if (order == 1) {
+            if (small_near) go(m2l_kernel<1, true>);
+            else go(m2l_kernel<1, false>);
+        } else {
+            if (small_near) go(m2l_kernel<0, true>);
+            else go(m2l_kernel<0, false>);
+        }
     };
-    if (order == 1) {
-        if (small_near) launch(m2l_kernel<1, true>);
-        else launch(m2l_kernel<1, false>);
+    // Full rounds of one 512-thread CTA per SM, then -- when the remainder
+    // would leave most SMs idle in a last round -- the remaining leaves split
+    // over several CTAs each (e.g. 512 leaves: 3 x 148 + 68 leaves as 136
+    // half-leaf CTAs).  Every target keeps its own sequential chain, so the
+    // bits do not depend on the launch shape.
+    const int64_t sms = sm_count();
+    const int64_t rem = nleaves % sms;
+    if (nleaves > sms && rem > 0 && 2 * rem <= sms) {
+        launch_range(0, nleaves - rem);
+        launch_range(nleaves - rem, rem);
     } else {
-        if (small_near) launch(m2l_kernel<0, true>);
-        else launch(m2l_kernel<0, false>);
+        launch_range(0, nleaves);
     }
     return sg_check_launch("sg_m2l");
 }
