@@ -348,7 +348,7 @@ def run_ours(args) -> None:
     barrier()
     gpu_uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
     u.timers = {}
-    launches0 = _lib.LAUNCHES["count"]
+    launches0 = _lib.launch_count()
     with ClockSampler(gpu_uuid) as clk:
         s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s_ev.record()
@@ -356,7 +356,7 @@ def run_ours(args) -> None:
             u.step()
         e_ev.record()
         barrier()
-    launches = _lib.LAUNCHES["count"] - launches0
+    launches = _lib.launch_count() - launches0
     elapsed = s_ev.elapsed_time(e_ev) * 1e-3
     u.check_errors()
     per_kernel = {}

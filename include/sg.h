@@ -45,6 +45,8 @@ extern "C" {
 int sg_abi_version(void);
 const char *sg_last_error(void);
 int sg_device_sm_count(void);
+/* kernels launched by this library so far (all threads, monotonic) */
+unsigned long long sg_launch_count(void);
 
 /* ---------------------------------------------------------------- gravity */
 

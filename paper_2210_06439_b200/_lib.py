@@ -21,6 +21,7 @@ _d = ctypes.c_double
 SIGNATURES = {
     "sg_abi_version": [],
     "sg_device_sm_count": [],
+    "sg_launch_count": [],
     "sg_cluster_aggregate": [_p, _i64, _i64, _i64, _i64, _d, _p, _p],
     "sg_p2p": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _d, _d, _i32,
                _p, _i64, _i64, _i64, _i64, _p],
@@ -43,7 +44,7 @@ SIGNATURES = {
 }
 
 
-RESTYPES = {"sg_m2l_workspace_bytes": _i64}
+RESTYPES = {"sg_m2l_workspace_bytes": _i64, "sg_launch_count": ctypes.c_ulonglong}
 
 
 class SGUnavailable(RuntimeError):
@@ -79,7 +80,12 @@ def load(path: Path | None = None):
     return L
 
 
-LAUNCHES = {"count": 0}  # kernels launched through call(); bench.py reads it
+LAUNCHES = {"count": 0}  # ABI calls made through call()
+
+
+def launch_count() -> int:
+    """Kernels actually launched by libsg.so (an ABI call may launch several)."""
+    return int(load().sg_launch_count())
 
 
 def call(name: str, *args) -> None:

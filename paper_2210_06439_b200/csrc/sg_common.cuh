@@ -74,4 +74,5 @@ __device__ __forceinline__ bool signbit_d(double v) {
 
 // error reporting shared by every C-ABI entry point
 void sg_set_error(const char* fmt, ...);
+void sg_count_launch(int n);
 int sg_check_launch(const char* what);

@@ -571,6 +571,7 @@ int sg_cluster_aggregate(const double* mass, int64_t mnx, int64_t mny, int64_t m
     const int64_t total = ncx * ncy * ncz * nleaf;
     if (total == 0) return SG_OK;
     // stacked blocks are contiguous, so treat them as one taller array
+    sg_count_launch(1);
     cluster_aggregate_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         mass, mnx, mny, ncx, ncy, ncz * nleaf, dx, reinterpret_cast<double4*>(clusters));
     return sg_check_launch("sg_cluster_aggregate");
@@ -623,6 +624,7 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
         const size_t smem = sizeof(double) * (size_t)S * S * p2p_pitch(S);
         cudaFuncSetAttribute(p2p_param_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int64_t pgrid = nleaves < 4 * sm_count() ? nleaves : 4 * sm_count();
+        sg_count_launch(1);
         p2p_param_kernel<<<(unsigned)pgrid, P2P_PARAM_THREADS, smem, (cudaStream_t)stream>>>(mv, leaves, nleaves,
                                                                                               halo, ov, st);
         return sg_check_launch("sg_p2p");
@@ -630,6 +632,7 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     const size_t smem = sizeof(P2PEntry) * P2P_THREADS + sizeof(int) * 32 +
                         sizeof(double) * (size_t)S * S * p2p_pitch(S);
     cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sg_count_launch(1);
     p2p_kernel<<<(unsigned)grid, P2P_THREADS, smem, (cudaStream_t)stream>>>(
         mv, leaves, nleaves, dx, rad2, eps2, halo, ov, out);
     return sg_check_launch("sg_p2p");
@@ -706,6 +709,7 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
         }
         auto go = [&](auto kern) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M2L_SMEM);
+            sg_count_launch(1);
             kern<<<(unsigned)grid, threads, M2L_SMEM, (cudaStream_t)stream>>>(mvr, cvr, lv, count, dx, rad2, eps2,
                                                                              i0, i1, ovr, workspace);
         };

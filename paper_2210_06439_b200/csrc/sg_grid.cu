@@ -17,6 +17,10 @@ void sg_set_error(const char* fmt, ...) {
     va_end(ap);
 }
 
+static unsigned long long g_launches = 0;  // kernels launched by this library
+
+void sg_count_launch(int n) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
+
 int sg_check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -111,6 +115,8 @@ extern "C" {
 
 int sg_abi_version(void) { return SG_ABI_VERSION; }
 
+unsigned long long sg_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
 const char* sg_last_error(void) { return g_err; }
 
 int sg_device_sm_count(void) {
@@ -131,6 +137,7 @@ int sg_fill_periodic(double* field, int64_t ncomp, int64_t nx, int64_t ny, int64
     const int64_t per = ((wrap_mask & 4) ? 2 * pad * Y * X : 0) + nz * 2 * pad * X + nz * ny * 2 * pad;
     const int64_t total = per * ncomp;
     if (total == 0 || pad == 0) return SG_OK;
+    sg_count_launch(1);
     fill_periodic_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         field, ncomp, nx, ny, nz, pad, wrap_mask);
     return sg_check_launch("sg_fill_periodic");
@@ -147,6 +154,7 @@ int sg_gather_blocks(const double* field, int64_t nx, int64_t ny, int64_t nz, in
     const int64_t total = (int64_t)S * S * S * ncomp * nleaves;
     if (total == 0) return SG_OK;
     FieldView v = make_view(field, nx, ny, nz, pad, leaf_stride);
+    sg_count_launch(1);
     gather_blocks_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(v, leaves, nleaves,
                                                                                             ncomp, halo, out);
     return sg_check_launch("sg_gather_blocks");
@@ -156,6 +164,7 @@ int sg_scale_copy(double* dst, int32_t dst_pad, const double* src, int32_t src_p
                   int64_t nz, double scale, void* stream) {
     const int64_t total = nx * ny * nz;
     if (total == 0) return SG_OK;
+    sg_count_launch(1);
     scale_copy_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         dst, dst_pad, src, src_pad, nx, ny, nz, scale);
     return sg_check_launch("sg_scale_copy");

@@ -670,6 +670,7 @@ int sg_reconstruct(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
     }
     FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
     dim3 grid((REC_CELLS + REC_THREADS - 1) / REC_THREADS, (unsigned)nleaves);
+    sg_count_launch(1);
     reconstruct_kernel<<<grid, REC_THREADS, 0, (cudaStream_t)stream>>>(uv, leaves, floor_, Q);
     return sg_check_launch("sg_reconstruct");
 }
@@ -679,6 +680,7 @@ int sg_flux(const double* Q, int64_t nleaves, double gamma, double* FX, double* 
     int rc = init_tables();
     if (rc) return rc;
     if (nleaves <= 0) return SG_OK;
+    sg_count_launch(1);
     flux_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax, err, latch);
     return sg_check_launch("sg_flux");
 }
@@ -688,6 +690,7 @@ int sg_flux_legacy(const double* Q, int64_t nleaves, double gamma, double* FX, d
     int rc = init_tables();
     if (rc) return rc;
     if (nleaves <= 0) return SG_OK;
+    sg_count_launch(1);
     flux_legacy_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax,
                                                                                       err, latch);
     return sg_check_launch("sg_flux_legacy");
@@ -713,6 +716,7 @@ int sg_hydro_fused(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t grid = nleaves < nsm ? nleaves : nsm;
+    sg_count_launch(1);
     hydro_fused_kernel<<<(unsigned)grid, FUSED_THREADS, FUSED_SMEM, (cudaStream_t)stream>>>(
         uv, leaves, nleaves, floor_, gamma, FX, FY, FZ, smax, err, latch);
     return sg_check_launch("sg_hydro_fused");
@@ -724,6 +728,7 @@ int sg_hydro_update(double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
                     double cfl, uint32_t* status, uint32_t* latch, void* stream) {
     if (nleaves <= 0) return SG_OK;
     FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
+    sg_count_launch(1);
     hydro_update_kernel<<<(unsigned)nleaves, 512, 0, (cudaStream_t)stream>>>(
         uv, leaves, FX, FY, FZ, smax, dt_dev, dt, dx, cfl, status, latch);
     return sg_check_launch("sg_hydro_update");
@@ -734,16 +739,19 @@ int sg_max_wavespeed(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_
                      void* stream) {
     if (nleaves <= 0) return SG_OK;
     FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
+    sg_count_launch(1);
     max_wavespeed_kernel<<<(unsigned)nleaves, 512, 0, (cudaStream_t)stream>>>(uv, leaves, gamma, pfloor, smax);
     return sg_check_launch("sg_max_wavespeed");
 }
 
 int sg_max_reduce(const double* vals, int64_t n, double* out, void* stream) {
+    sg_count_launch(1);
     max_reduce_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(vals, n, out);
     return sg_check_launch("sg_max_reduce");
 }
 
 int sg_dt_from_smax(const double* s_pre, double cfl, double dx, double* dt, void* stream) {
+    sg_count_launch(1);
     dt_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(s_pre, cfl, dx, dt);
     return sg_check_launch("sg_dt_from_smax");
 }

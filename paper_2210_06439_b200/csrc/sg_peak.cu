@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(int iters, double a, dou
 
 extern "C" int sg_fp64_peak(int mode, int iters, double* sink, int64_t* flops_out, void* stream) {
     const int grid = 4 * sg_device_sm_count();
+    sg_count_launch(1);
     if (mode == 0)
         sg::fp64_peak_kernel<0><<<grid, 256, 0, (cudaStream_t)stream>>>(iters, 1e-3, 0.999999, sink);
     else

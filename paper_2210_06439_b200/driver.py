@@ -194,7 +194,7 @@ def run_scenario(cfg: ScenarioConfig, backend: str = "scalar", threads: int = 1,
                       legacy_flux=hydro_kernel == "legacy")
     st.load({name: global_field(tree, name) for name in HYDRO_FIELDS})
     st.timers = {}
-    launches0 = _lib.LAUNCHES["count"]
+    launches0 = _lib.launch_count()
     torch.cuda.synchronize()
     t0 = time.perf_counter_ns()
     for step in range(cfg.stop_step):
@@ -231,7 +231,7 @@ def run_scenario(cfg: ScenarioConfig, backend: str = "scalar", threads: int = 1,
         set_global_field(tree, "mass", st.mass[p:p + st.nz, p:p + st.n, p:p + st.n].cpu().numpy())
     return RunResult(config=cfg, backend=bk.name, threads=threads, tasks_per_multipole=tasks_per_multipole,
                      tree=tree, records=records, computation_s=total_ns / 1e9,
-                     launch_stats=LaunchStats(gpu_launches=_lib.LAUNCHES["count"] - launches0))
+                     launch_stats=LaunchStats(gpu_launches=_lib.launch_count() - launches0))
 
 
 def bench_records(result: RunResult) -> list:
