@@ -36,7 +36,15 @@
 extern "C" {
 #endif
 
-#define SG_ABI_VERSION 1
+#define SG_ABI_VERSION 2
+
+/* precision modes of the gravity kernels:
+ *  SG_PREC_EXACT  bit-identical to the reference (no FMA, reference order)
+ *  SG_PREC_FMA    FMA-contracted / re-associated far terms (north_star's
+ *                 FP64 FMA design); within 1e-12 max-norm relative per output
+ *                 component of the exact results (tests/test_gpu_fma.py) */
+#define SG_PREC_EXACT 0
+#define SG_PREC_FMA 1
 
 #define SG_OK 0
 #define SG_EINVAL 1
@@ -65,7 +73,8 @@ int sg_cluster_aggregate(const double *mass, int64_t mnx, int64_t mny, int64_t m
  * (phi, gx, gy, gz), pad 0, dims (onx, ony, onz). */
 int sg_p2p(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
            const int32_t *leaves, int64_t nleaves, double dx, double rad2, double eps2, int32_t halo,
-           double *out, int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, void *stream);
+           double *out, int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, int32_t precision,
+           void *stream);
 
 /* Replaces compiled.multipole_kernel_impl (compiled.py:355-451) called by
  * kernels.multipole_prepare/multipole_kernel (kernels/__init__.py:224-261).
@@ -80,7 +89,7 @@ int sg_m2l(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
            const double *clusters, int64_t cluster_leaf_stride, const int32_t *leaves, int64_t nleaves,
            double dx, double rad2, double eps2, int32_t order, int32_t i0, int32_t i1, double *out,
            int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, double *workspace,
-           int64_t workspace_bytes, void *stream);
+           int64_t workspace_bytes, int32_t precision, void *stream);
 
 /* ------------------------------------------------------------------ hydro */
 

@@ -10,7 +10,7 @@ import ctypes
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libsg.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -24,9 +24,9 @@ SIGNATURES = {
     "sg_launch_count": [],
     "sg_cluster_aggregate": [_p, _i64, _i64, _i64, _i64, _d, _p, _p],
     "sg_p2p": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _d, _d, _i32,
-               _p, _i64, _i64, _i64, _i64, _p],
+               _p, _i64, _i64, _i64, _i64, _i32, _p],
     "sg_m2l": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _p, _i64, _d, _d, _d, _i32, _i32, _i32,
-               _p, _i64, _i64, _i64, _i64, _p, _i64, _p],
+               _p, _i64, _i64, _i64, _i64, _p, _i64, _i32, _p],
     "sg_m2l_workspace_bytes": [_i64],
     "sg_reconstruct": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _p, _p],
     "sg_flux": [_p, _i64, _d, _p, _p, _p, _p, _p, _p, _p],
@@ -56,6 +56,9 @@ class SGError(RuntimeError):
 
 
 _lib = None
+
+PREC_EXACT, PREC_FMA = 0, 1
+PRECISIONS = {"exact": PREC_EXACT, "fma": PREC_FMA}
 
 
 def load(path: Path | None = None):

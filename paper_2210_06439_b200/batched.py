@@ -70,11 +70,20 @@ def cluster_aggregate(mass: torch.Tensor, dx: float, clusters: torch.Tensor, nle
     _lib.call("sg_cluster_aggregate", _f64(mass), mnx, mny, mnz, nleaf, float(dx), _f64(clusters), _stream())
 
 
+def _prec(precision) -> int:
+    if isinstance(precision, str):
+        try:
+            return _lib.PRECISIONS[precision]
+        except KeyError:
+            raise ValueError(f"precision must be one of {sorted(_lib.PRECISIONS)}, got {precision!r}") from None
+    return int(precision)
+
+
 def p2p(mass, mv: View, leaves, nleaves: int, dx: float, rad2: float, eps2: float, halo: int,
-        out, ov: View) -> None:
+        out, ov: View, precision="exact") -> None:
     _lib.call("sg_p2p", _f64(mass), mv.nx, mv.ny, mv.nz, mv.pad, mv.leaf_stride, _ptr(leaves), nleaves,
               float(dx), float(rad2), float(eps2), int(halo), _f64(out), ov.nx, ov.ny, ov.nz,
-              ov.leaf_stride, _stream())
+              ov.leaf_stride, _prec(precision), _stream())
 
 
 _WORKSPACE: dict = {}
@@ -92,12 +101,13 @@ def m2l_workspace(nleaves: int, device=None) -> torch.Tensor:
 
 
 def m2l(mass, mv: View, clusters, cluster_leaf_stride: int, leaves, nleaves: int, dx: float, rad2: float,
-        eps2: float, order: int, out, ov: View, i0: int = 0, i1: int = 512, workspace=None) -> None:
+        eps2: float, order: int, out, ov: View, i0: int = 0, i1: int = 512, workspace=None,
+        precision="exact") -> None:
     ws = workspace if workspace is not None else m2l_workspace(nleaves, mass.device)
     _lib.call("sg_m2l", _f64(mass), mv.nx, mv.ny, mv.nz, mv.pad, mv.leaf_stride, _f64(clusters),
               cluster_leaf_stride, _ptr(leaves), nleaves, float(dx), float(rad2), float(eps2), int(order),
               int(i0), int(i1), _f64(out), ov.nx, ov.ny, ov.nz, ov.leaf_stride, _f64(ws), ws.numel() * 8,
-              _stream())
+              _prec(precision), _stream())
 
 
 def reconstruct(U, uv: View, leaves, nleaves: int, floor: float, Q) -> None:

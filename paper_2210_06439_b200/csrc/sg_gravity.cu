@@ -120,6 +120,7 @@ __device__ int p2p_build_chunk(P2PEntry* ent, int* warp_cnt, int c0, int halo, d
 // two targets per thread, (x, y, z) and (x, y, z + 4): each uniform stencil
 // entry is loaded once for both (the kernel is issue-bound)
 constexpr int P2P_PARAM_THREADS = 256;
+template <bool FAST>
 __global__ void __launch_bounds__(P2P_PARAM_THREADS, 4)
 p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, int halo, FieldView ov,
                  const __grid_constant__ P2PStencil st) {
@@ -148,14 +149,25 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
             const double inv = st.inv[e], inv3 = st.inv3[e], rx = st.rx[e], ry = st.ry[e], rz = st.rz[e];
             const double ma = cube[tcell + d], mb = cube[t2 + d];
             const double ca = mul(ma, inv3), cb = mul(mb, inv3);
-            ap = add(ap, -mul(ma, inv));
-            ax = add(ax, -mul(ca, rx));
-            ay = add(ay, -mul(ca, ry));
-            az = add(az, -mul(ca, rz));
-            bp = add(bp, -mul(mb, inv));
-            bx = add(bx, -mul(cb, rx));
-            by = add(by, -mul(cb, ry));
-            bz = add(bz, -mul(cb, rz));
+            if (FAST) {  // FMA-contracted: 5 DP instructions per pair instead of 9
+                ap = __fma_rn(-ma, inv, ap);
+                ax = __fma_rn(-ca, rx, ax);
+                ay = __fma_rn(-ca, ry, ay);
+                az = __fma_rn(-ca, rz, az);
+                bp = __fma_rn(-mb, inv, bp);
+                bx = __fma_rn(-cb, rx, bx);
+                by = __fma_rn(-cb, ry, by);
+                bz = __fma_rn(-cb, rz, bz);
+            } else {
+                ap = add(ap, -mul(ma, inv));
+                ax = add(ax, -mul(ca, rx));
+                ay = add(ay, -mul(ca, ry));
+                az = add(az, -mul(ca, rz));
+                bp = add(bp, -mul(mb, inv));
+                bx = add(bx, -mul(cb, rx));
+                by = add(by, -mul(cb, ry));
+                bz = add(bz, -mul(cb, rz));
+            }
         }
         double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy + x;
         o[0] = ap;
@@ -330,12 +342,35 @@ __device__ __forceinline__ int cluster_of(int t, int a) {
     return (u & 1) ? (t + 8 + a) >> 1 : u >> 1;
 }
 
-template <int ORDER>
+// FAST (precision = SG_PREC_FMA): the same far term FMA-contracted and
+// re-associated, 13 DP instructions instead of 30 (order 1):
+//   g = D inv3 - (gcom + 3 dr inv5) r,   p = -(M inv) - dr inv3
+// folded into the accumulators; the FAST table holds 3 inv5 in the inv5 slot.
+// Results stay within 1e-12 max-norm relative of the exact path (tests).
+template <int ORDER, bool FAST>
 __device__ __forceinline__ void m2l_far(const double* __restrict__ row, int ax, const double4& c, double rx,
                                         double ry, double rz, double& acc_p, double& acc_x, double& acc_y,
                                         double& acc_z) {
     const double inv = row[ax];
     const double inv3 = row[16 + ax];
+    if (FAST) {
+        const double gcom = mul(c.x, inv3);
+        if (ORDER == 1) {
+            const double i5x3 = row[32 + ax];
+            const double dr = __fma_rn(c.w, rz, __fma_rn(c.z, ry, mul(c.y, rx)));
+            acc_p = __fma_rn(-dr, inv3, __fma_rn(-c.x, inv, acc_p));
+            const double sg = __fma_rn(dr, i5x3, gcom);
+            acc_x = __fma_rn(c.y, inv3, __fma_rn(-sg, rx, acc_x));
+            acc_y = __fma_rn(c.z, inv3, __fma_rn(-sg, ry, acc_y));
+            acc_z = __fma_rn(c.w, inv3, __fma_rn(-sg, rz, acc_z));
+        } else {
+            acc_p = __fma_rn(-c.x, inv, acc_p);
+            acc_x = __fma_rn(-gcom, rx, acc_x);
+            acc_y = __fma_rn(-gcom, ry, acc_y);
+            acc_z = __fma_rn(-gcom, rz, acc_z);
+        }
+        return;
+    }
     double p_f = -mul(c.x, inv);
     const double gcom = mul(c.x, inv3);
     double gx_f = -mul(gcom, rx);
@@ -356,7 +391,7 @@ __device__ __forceinline__ void m2l_far(const double* __restrict__ row, int ax, 
     acc_z = add(acc_z, gz_f);
 }
 
-template <int ORDER, bool SMALL_NEAR>
+template <int ORDER, bool SMALL_NEAR, bool FAST>
 __global__ void __launch_bounds__(M2L_THREADS, 1)
 m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int64_t B, double dx,
            double rad2, double eps2, int i0, int i1, FieldView ov, double* __restrict__ work) {
@@ -390,7 +425,8 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
             const double inv3 = mul(mul(inv, inv), inv);
             row[ax] = inv;
             row[16 + ax] = inv3;
-            row[32 + ax] = mul(mul(inv3, inv), inv);
+            const double inv5 = mul(mul(inv3, inv), inv);
+            row[32 + ax] = FAST ? mul(3.0, inv5) : inv5;
         } else {
             row[ax] = -1.0;  // near marker (sign bit); near path computes its own terms
             row[16 + ax] = 0.0;
@@ -492,7 +528,7 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
                 if (!__any_sync(0xffffffffu, signbit_d(row[0]))) {
 #pragma unroll
                     for (int cx = 0; cx < NC; ++cx)
-                        m2l_far<ORDER>(row, axv[cx], crow[cx], rxv[cx], ry, rz, acc_p, acc_x, acc_y, acc_z);
+                        m2l_far<ORDER, FAST>(row, axv[cx], crow[cx], rxv[cx], ry, rz, acc_p, acc_x, acc_y, acc_z);
                 } else if (SMALL_NEAR) {
                     // rows holding near clusters: far term for every cluster,
                     // near lanes take their prologue sum instead (same order)
@@ -500,7 +536,7 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
 #pragma unroll
                     for (int cx = 0; cx < NC; ++cx) {
                         double p = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
-                        m2l_far<ORDER>(row, axv[cx], crow[cx], rxv[cx], ry, rz, p, gx, gy, gz);
+                        m2l_far<ORDER, FAST>(row, axv[cx], crow[cx], rxv[cx], ry, rz, p, gx, gy, gz);
                         if (signbit_d(row[axv[cx]])) {
                             const int k = near_slot[rowslot + axv[cx]];
                             p = wk[(k * 4 + 0) * M2L_THREADS];
@@ -519,7 +555,7 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
                         const int ax = fold(x - 2 * cx + 7);
                         if (!signbit_d(row[ax])) {
                             const double rx = mul(sub(tx, add((double)(2 * cx - 8), 1.0)), dx);
-                            m2l_far<ORDER>(row, ax, crow[cx], rx, ry, rz, acc_p, acc_x, acc_y, acc_z);
+                            m2l_far<ORDER, FAST>(row, ax, crow[cx], rx, ry, rz, acc_p, acc_x, acc_y, acc_z);
                         } else {
                             double r[4];
                             m2l_near(mc, mv.sy, mv.sz, near_tab, x, y, z, cx, cy, cz, dx, eps2, r);
@@ -579,7 +615,8 @@ int sg_cluster_aggregate(const double* mass, int64_t mnx, int64_t mny, int64_t m
 
 int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
            const int32_t* leaves, int64_t nleaves, double dx, double rad2, double eps2, int32_t halo,
-           double* out, int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, void* stream) {
+           double* out, int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, int32_t precision,
+           void* stream) {
     if (halo < 0 || halo > 8 || halo > pad) {
         sg_set_error("sg_p2p: halo %d must be in [0, min(8, pad=%d)]", halo, pad);
         return SG_EINVAL;
@@ -622,11 +659,15 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
             }
         }
         const size_t smem = sizeof(double) * (size_t)S * S * p2p_pitch(S);
-        cudaFuncSetAttribute(p2p_param_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int64_t pgrid = nleaves < 4 * sm_count() ? nleaves : 4 * sm_count();
-        sg_count_launch(1);
-        p2p_param_kernel<<<(unsigned)pgrid, P2P_PARAM_THREADS, smem, (cudaStream_t)stream>>>(mv, leaves, nleaves,
-                                                                                              halo, ov, st);
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            sg_count_launch(1);
+            kern<<<(unsigned)pgrid, P2P_PARAM_THREADS, smem, (cudaStream_t)stream>>>(mv, leaves, nleaves, halo, ov,
+                                                                                     st);
+        };
+        if (precision == SG_PREC_FMA) go(p2p_param_kernel<true>);
+        else go(p2p_param_kernel<false>);
         return sg_check_launch("sg_p2p");
     }
     const size_t smem = sizeof(P2PEntry) * P2P_THREADS + sizeof(int) * 32 +
@@ -667,13 +708,17 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
            const double* clusters, int64_t cluster_leaf_stride, const int32_t* leaves, int64_t nleaves,
            double dx, double rad2, double eps2, int32_t order, int32_t i0, int32_t i1, double* out,
            int64_t onx, int64_t ony, int64_t onz, int64_t out_leaf_stride, double* workspace,
-           int64_t workspace_bytes, void* stream) {
+           int64_t workspace_bytes, int32_t precision, void* stream) {
     if (pad < 8 || (pad & 1)) {
         sg_set_error("sg_m2l: mass pad must be even and >= 8 (got %d)", pad);
         return SG_EINVAL;
     }
     if (order != 0 && order != 1) {
         sg_set_error("sg_m2l: expansion order must be 0 or 1 (got %d)", order);
+        return SG_EINVAL;
+    }
+    if (precision != SG_PREC_EXACT && precision != SG_PREC_FMA) {
+        sg_set_error("sg_m2l: unknown precision mode %d", precision);
         return SG_EINVAL;
     }
     if (nleaves <= 0 || i1 <= i0) return SG_OK;
@@ -713,12 +758,13 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
             kern<<<(unsigned)grid, threads, M2L_SMEM, (cudaStream_t)stream>>>(mvr, cvr, lv, count, dx, rad2, eps2,
                                                                              i0, i1, ovr, workspace);
         };
+        const bool fast = precision == SG_PREC_FMA;
         if (order == 1) {
-            if (small_near) go(m2l_kernel<1, true>);
-            else go(m2l_kernel<1, false>);
+            if (small_near) fast ? go(m2l_kernel<1, true, true>) : go(m2l_kernel<1, true, false>);
+            else fast ? go(m2l_kernel<1, false, true>) : go(m2l_kernel<1, false, false>);
         } else {
-            if (small_near) go(m2l_kernel<0, true>);
-            else go(m2l_kernel<0, false>);
+            if (small_near) fast ? go(m2l_kernel<0, true, true>) : go(m2l_kernel<0, true, false>);
+            else fast ? go(m2l_kernel<0, false, true>) : go(m2l_kernel<0, false, false>);
         }
     };
     // Full rounds of one 512-thread CTA per SM, then -- when the remainder

@@ -37,7 +37,7 @@ class UnigridState:
 
     def __init__(self, level: int, hydro: HydroConfig | None = None, gravity: GravityConfig | None = None,
                  slab: Slab | None = None, device=None, group=None, fused_hydro: bool = True,
-                 legacy_flux: bool = False):
+                 legacy_flux: bool = False, precision: str = "exact"):
         B.require_device()
         self.level = level
         self.slab = slab or Slab(level)
@@ -46,6 +46,11 @@ class UnigridState:
         self.h = hydro or HydroConfig()
         self.g = gravity or GravityConfig(expansion_order=1)
         self.group = group
+        # gravity arithmetic: "exact" = bit-identical to the reference;
+        # "fma" = FMA-contracted far/near terms within 1e-12 (include/sg.h)
+        if precision not in ("exact", "fma"):
+            raise ValueError(f"precision must be 'exact' or 'fma', got {precision!r}")
+        self.precision = precision
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         n, nz = self.slab.n, self.slab.nz
         self.n, self.nz = n, nz
@@ -196,11 +201,11 @@ class UnigridState:
         self._done(ev)
         ev = self._t("p2p")
         B.p2p(self.mass, self.mv, self.leaves, self.nleaves, self.dx, self.rad2, self.eps2, self.halo,
-              self.grav, self.gv)
+              self.grav, self.gv, precision=self.precision)
         self._done(ev)
         ev = self._t("m2l")
         B.m2l(self.mass, self.mv, self.clusters, 0, self.leaves, self.nleaves, self.dx, self.rad2, self.eps2,
-              self.g.expansion_order, self.grav, self.gv)
+              self.g.expansion_order, self.grav, self.gv, precision=self.precision)
         self._done(ev)
 
     def wavespeed_dt(self) -> None:

@@ -19,7 +19,7 @@ def test_library_exports_every_header_symbol():
     lib = ctypes.CDLL(str(REPO / "paper_2210_06439_b200" / "libsg.so"))
     missing = [s for s in sorted(header_symbols()) if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.sg_abi_version() == 1
+    assert lib.sg_abi_version() == 2
 
 
 def test_binding_table_covers_header():
