@@ -12,8 +12,10 @@ from paper_2210_06439_b200.kernels import GravityConfig, HydroConfig  # noqa: E4
 
 what = sys.argv[1] if len(sys.argv) > 1 else "all"
 level = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+prec = sys.argv[3] if len(sys.argv) > 3 else "exact"
 if what in ("gravity", "all"):
-    u = grid.UnigridState(level, HydroConfig(), GravityConfig(theta=0.34, eps=0.5, expansion_order=1))
+    u = grid.UnigridState(level, HydroConfig(), GravityConfig(theta=0.34, eps=0.5, expansion_order=1),
+                          precision=prec)
     rho = scenarios.polytrope_rho(level, 1e-10)
     z = torch.zeros_like(torch.from_numpy(rho))
     u.load({"rho": rho, "sx": z.numpy(), "sy": z.numpy(), "sz": z.numpy(), "E": rho})
