@@ -27,7 +27,9 @@ __constant__ int c_dminus[3][9];
 // geometry.py:59-61
 __constant__ double c_simpson[9];
 
-static bool g_tables_ready = false;
+// __constant__ memory is per device: upload the tables once per device
+constexpr int SG_MAX_DEVICES = 64;
+static bool g_tables_ready[SG_MAX_DEVICES] = {};
 
 static int host_dir_index(int dz, int dy, int dx) {
     int idx = (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
@@ -35,7 +37,12 @@ static int host_dir_index(int dz, int dy, int dx) {
 }
 
 static int init_tables() {
-    if (g_tables_ready) return SG_OK;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= SG_MAX_DEVICES) {
+        sg_set_error("hydro constant tables: no current CUDA device");
+        return SG_ECUDA;
+    }
+    if (g_tables_ready[dev]) return SG_OK;
     double dirs[NDIR][3];
     int d = 0;
     for (int dz = -1; dz <= 1; ++dz)
@@ -69,7 +76,7 @@ static int init_tables() {
         sg_set_error("hydro constant tables: %s", cudaGetErrorString(cudaGetLastError()));
         return SG_ECUDA;
     }
-    g_tables_ready = true;
+    g_tables_ready[dev] = true;
     return SG_OK;
 }
 

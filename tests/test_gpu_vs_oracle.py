@@ -1,0 +1,104 @@
+"""Randomised parity: CUDA path vs the CPU oracle (bit-pinned to the
+reference by tests/test_oracle_golden.py) on seeded inputs outside the
+fixtures -- non-power-of-two cell widths, varied theta / eps / order, varied
+gamma / floor, NaN-poisoned inputs.  Bitwise (NaNs compared as NaNs)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+from paper_2210_06439_b200 import batched as B  # noqa: E402
+from paper_2210_06439_b200 import kernels as K  # noqa: E402
+from paper_2210_06439_b200.batched import View  # noqa: E402
+
+
+def same(a, b) -> bool:
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    na, nb = np.isnan(a), np.isnan(b)
+    return a.shape == b.shape and np.array_equal(na, nb) and np.array_equal(a[~na].view(np.uint64),
+                                                                             b[~nb].view(np.uint64))
+
+
+CASES = [(1.0 / 64, 0.34, 0.5, 1), (0.1, 0.34, 0.5, 1), (1.0 / 3.0, 0.5, 0.25, 0), (7.0, 0.27, 1.5, 1),
+         (1e-3, 0.34, 0.5, 0), (0.05, 0.2, 0.5, 1)]
+
+
+@pytest.mark.parametrize("dx,theta,eps,order", CASES)
+def test_m2l_p2p_random_cubes(dx, theta, eps, order):
+    rng = np.random.default_rng(int(dx * 1e6) + int(theta * 100))
+    cube = rng.lognormal(0.0, 1.0, (24, 24, 24)) * dx ** 3
+    cube[rng.uniform(size=cube.shape) < 0.05] = 0.0
+    d = torch.from_numpy(cube).cuda()
+    cl = torch.empty((12, 12, 12, 4), dtype=torch.float64, device="cuda")
+    B.cluster_aggregate(d, dx, cl)
+    cfg = K.GravityConfig(theta=theta, eps=eps, expansion_order=order)
+    rad2, eps2 = K.gravity_params(dx, cfg)
+    out = torch.zeros((4, 8, 8, 8), dtype=torch.float64, device="cuda")
+    B.m2l(d, View(8, 8, 8, 8), cl, 0, None, 1, dx, rad2, eps2, order, out, View(8, 8, 8, 0))
+    assert same(out.cpu().numpy(), O.multipole(cube, dx, theta, eps, order))
+    h = K.gravity_halo(theta)
+    sub = np.ascontiguousarray(cube[8 - h:16 + h, 8 - h:16 + h, 8 - h:16 + h])
+    out.zero_()
+    B.p2p(torch.from_numpy(sub).cuda(), View(8, 8, 8, h), None, 1, dx, rad2, eps2, h, out, View(8, 8, 8, 0))
+    assert same(out.cpu().numpy(), O.monopole(sub, dx, theta, eps))
+
+
+def test_m2l_nan_and_inf_masses_propagate_like_reference():
+    rng = np.random.default_rng(9)
+    cube = rng.lognormal(0.0, 1.0, (24, 24, 24))
+    cube[3, 4, 5] = np.nan        # a far cluster
+    cube[12, 11, 12] = np.inf     # a near cell of central targets
+    d = torch.from_numpy(cube).cuda()
+    cl = torch.empty((12, 12, 12, 4), dtype=torch.float64, device="cuda")
+    B.cluster_aggregate(d, 1.0 / 64, cl)
+    rad2, eps2 = K.gravity_params(1.0 / 64, K.GravityConfig())
+    out = torch.zeros((4, 8, 8, 8), dtype=torch.float64, device="cuda")
+    B.m2l(d, View(8, 8, 8, 8), cl, 0, None, 1, 1.0 / 64, rad2, eps2, 1, out, View(8, 8, 8, 0))
+    assert same(out.cpu().numpy(), O.multipole(cube, 1.0 / 64, 0.34, 0.5, 1))
+
+
+@pytest.mark.parametrize("gamma,floor,seed", [(1.4, 1e-12, 1), (5.0 / 3.0, 1e-6, 2), (1.1, 1e-3, 3), (2.0, 1e-9, 4)])
+def test_hydro_random_blocks(gamma, floor, seed):
+    rng = np.random.default_rng(seed)
+    nb = 8
+    blocks = []
+    for i in range(nb):
+        scale = float(2.0 ** rng.integers(-8, 9)) * (1.0 + rng.uniform())
+        rho = (1.0 + 0.5 * rng.uniform(-1, 1, (12, 12, 12))) * scale
+        v = rng.uniform(-1, 1, (3, 12, 12, 12))
+        p = (1.0 + 0.5 * rng.uniform(-1, 1, (12, 12, 12))) * scale
+        U = np.stack([rho, rho * v[0], rho * v[1], rho * v[2], p / (gamma - 1.0) + 0.5 * rho * (v ** 2).sum(0)])
+        if i == 5:
+            U[4] *= 0.001          # energies clamped by the reconstruction floor
+        if i == 6:
+            U[0, 7, 3, 4] = np.nan  # poison reaches the interior
+        blocks.append(U)
+    Ud = torch.from_numpy(np.stack(blocks)).cuda()
+    v = View(8, 8, 8, 2, leaf_stride=5 * 1728)
+    Q = torch.empty((nb, 5, 26, 1000), dtype=torch.float64, device="cuda")
+    B.reconstruct(Ud, v, None, nb, floor, Q)
+    FX = torch.empty((nb, 5, 8, 8, 9), dtype=torch.float64, device="cuda")
+    FY = torch.empty((nb, 5, 8, 9, 8), dtype=torch.float64, device="cuda")
+    FZ = torch.empty((nb, 5, 9, 8, 8), dtype=torch.float64, device="cuda")
+    smax = torch.empty(nb, dtype=torch.float64, device="cuda")
+    err = torch.empty(nb, dtype=torch.int32, device="cuda")
+    B.flux(Q, nb, gamma, FX, FY, FZ, smax, err)
+    ws = torch.empty(nb, dtype=torch.float64, device="cuda")
+    B.max_wavespeed(Ud, v, None, nb, gamma, floor, ws)
+    Qh, FXh, FYh, FZh = (t.cpu().numpy() for t in (Q, FX, FY, FZ))
+    for i, U in enumerate(blocks):
+        Qw = O.reconstruct(U, floor)
+        assert same(Qh[i].reshape(Qw.shape), Qw), i
+        fx, fy, fz, s, code, cell = O.flux(Qw, gamma)
+        assert same(FXh[i], fx) and same(FYh[i], fy) and same(FZh[i], fz), i
+        assert K.decode_flux_error(int(err[i].cpu().numpy().view(np.uint32))) == (code, cell), i
+        assert same(smax[i].item(), s) and same(ws[i].item(), O.max_wavespeed(U, gamma, floor)), i
+    # fused path on the same blocks
+    FX2, FZ2 = torch.empty_like(FX), torch.empty_like(FZ)
+    B.hydro_fused(Ud, v, None, nb, floor, gamma, FX2, FY, FZ2, smax, err)
+    assert same(FX2.cpu().numpy(), FXh) and same(FZ2.cpu().numpy(), FZh)
