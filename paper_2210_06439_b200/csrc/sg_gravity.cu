@@ -578,6 +578,199 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
     }
 }
 
+// ---------------------------------------------------------------------------
+// FMA-mode M2L with mirror pairing.  With precision = SG_PREC_FMA the
+// accumulation order is free, so each thread owns two targets, x and 7-x (same
+// y, z): cluster cx for the first and cluster 11-cx for the second have the
+// same (|kx|,|ky|,|kz|) -> one geometry-table fetch serves two pairs, and
+// r_x of the second is -r_x of the first.  Halves the shared-memory table
+// traffic that bounds the one-target kernel in this mode.  256 threads = 512
+// targets per CTA; small-near regime only (theta >= ~0.28).
+// ---------------------------------------------------------------------------
+constexpr int MIR_THREADS = 256;
+constexpr int MIR_PITCH = 52;   // 104 words == 8 mod 32: a half-warp's 4 rows x 4 entries tile the banks
+constexpr size_t MIR_SMEM = sizeof(double) * TAB_N * TAB_N * MIR_PITCH + sizeof(double2) * NEAR_R * NEAR_R * NEAR_R +
+                            sizeof(double4) * NC * NC * NC + sizeof(double) * NBW * NBW * NBW + sizeof(int) * 32;
+constexpr int64_t MIR_WORK_PER_CTA = 27 * 4 * 2 * MIR_THREADS;  // doubles: [slot][comp][target][thread]
+
+template <int ORDER>
+__device__ __forceinline__ void mir_far(const double4& c, double inv, double inv3, double i5x3, double rx, double ry,
+                                        double rz, double& ap, double& ax, double& ay, double& az) {
+    const double gcom = mul(c.x, inv3);
+    if (ORDER == 1) {
+        const double dr = __fma_rn(c.w, rz, __fma_rn(c.z, ry, mul(c.y, rx)));
+        ap = __fma_rn(-dr, inv3, __fma_rn(-c.x, inv, ap));
+        const double sg = __fma_rn(dr, i5x3, gcom);
+        ax = __fma_rn(c.y, inv3, __fma_rn(-sg, rx, ax));
+        ay = __fma_rn(c.z, inv3, __fma_rn(-sg, ry, ay));
+        az = __fma_rn(c.w, inv3, __fma_rn(-sg, rz, az));
+    } else {
+        ap = __fma_rn(-c.x, inv, ap);
+        ax = __fma_rn(-gcom, rx, ax);
+        ay = __fma_rn(-gcom, ry, ay);
+        az = __fma_rn(-gcom, rz, az);
+    }
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(MIR_THREADS, 1)
+m2l_mirror_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int64_t B, double dx,
+                  double rad2, double eps2, FieldView ov, double* __restrict__ work) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* tab = reinterpret_cast<double*>(smem_raw);
+    double2* near_tab = reinterpret_cast<double2*>(tab + TAB_N * TAB_N * MIR_PITCH);
+    double4* cl = reinterpret_cast<double4*>(near_tab + NEAR_R * NEAR_R * NEAR_R);
+    double* nm = reinterpret_cast<double*>(cl + NC * NC * NC);
+    int* near_slot = reinterpret_cast<int*>(nm + NBW * NBW * NBW);
+    const int tid = threadIdx.x;
+    double* wk = work + (int64_t)blockIdx.x * MIR_WORK_PER_CTA + tid;
+
+    for (int e = tid; e < TAB_N * TAB_N * TAB_N; e += MIR_THREADS) {
+        const int ax = e % TAB_N, ay = (e / TAB_N) % TAB_N, az = e / (TAB_N * TAB_N);
+        const double rx = mul(add((double)ax, 0.5), dx);
+        const double ry = mul(add((double)ay, 0.5), dx);
+        const double rz = mul(add((double)az, 0.5), dx);
+        const double r2 = add(add(mul(rx, rx), mul(ry, ry)), mul(rz, rz));
+        double* row = tab + (az * TAB_N + ay) * MIR_PITCH;
+        if (r2 > rad2) {
+            const double inv = dvd(1.0, dsqrt(add(r2, eps2)));
+            const double inv3 = mul(mul(inv, inv), inv);
+            row[ax] = inv;
+            row[15 + ax] = inv3;
+            row[30 + ax] = mul(3.0, mul(mul(inv3, inv), inv));
+        } else {
+            row[ax] = -1.0;
+            row[15 + ax] = 0.0;
+            row[30 + ax] = 0.0;
+        }
+    }
+    for (int e = tid; e < NEAR_R * NEAR_R * NEAR_R; e += MIR_THREADS) {
+        const int ix = e % NEAR_R, iy = (e / NEAR_R) % NEAR_R, iz = e / (NEAR_R * NEAR_R);
+        const double sx = mul((double)ix, dx), sy = mul((double)iy, dx), sz = mul((double)iz, dx);
+        const double r2s = add(add(mul(sx, sx), mul(sy, sy)), mul(sz, sz));
+        near_tab[e] = r2s > 0.0 ? make_double2(dvd(1.0, dsqrt(add(r2s, eps2))), 0.0) : make_double2(-1.0, 0.0);
+        if (r2s > 0.0) near_tab[e].y = mul(mul(near_tab[e].x, near_tab[e].x), near_tab[e].x);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int k = 0;
+        for (int e = 0; e < 27; ++e) {
+            const int ax = e % 3, ay = (e / 3) % 3, az = e / 9;
+            near_slot[e] = signbit_d(tab[(az * TAB_N + ay) * MIR_PITCH + ax]) ? k++ : -1;
+        }
+    }
+
+    const int xa = tid & 3, y = (tid >> 2) & 7, z = tid >> 5;
+    const int xb = 7 - xa;
+    const double txa = (double)xa + 0.5, ty = (double)y + 0.5, tz = (double)z + 0.5;
+    double rxv[NC];
+    int axv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        rxv[c] = mul(sub(txa, add((double)(2 * c - 8), 1.0)), dx);
+        axv[c] = fold(xa - 2 * c + 7);
+    }
+
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        __syncthreads();
+        {
+            int64_t cx0 = cv.off, cy0 = cv.off, cz0 = cv.off;
+            if (leaves) {
+                cx0 += 4 * (int64_t)leaves[3 * b];
+                cy0 += 4 * (int64_t)leaves[3 * b + 1];
+                cz0 += 4 * (int64_t)leaves[3 * b + 2];
+            }
+            const double4* src = cv.base + b * cv.leaf_stride + cz0 * cv.sz + cy0 * cv.sy + cx0;
+            for (int i = tid; i < NC * NC * NC; i += MIR_THREADS) {
+                const int cx = i % NC, cy = (i / NC) % NC, cz = i / (NC * NC);
+                const double2* s2 = reinterpret_cast<const double2*>(src + cz * cv.sz + cy * cv.sy + cx);
+                const double2 a = __ldg(s2), c2 = __ldg(s2 + 1);
+                cl[i] = make_double4(a.x, a.y, c2.x, c2.y);
+            }
+        }
+        const double* mc = leaf_origin(mv, leaves, b, 8);
+        for (int i = tid; i < NBW * NBW * NBW; i += MIR_THREADS) {
+            const int cx = i % NBW, cy = (i / NBW) % NBW, cz = i / (NBW * NBW);
+            nm[i] = __ldg(mc + (int64_t)(cz + NB0) * mv.sz + (int64_t)(cy + NB0) * mv.sy + (cx + NB0));
+        }
+        __syncthreads();
+        // near-field sums of both targets (same (|kx|,|ky|,|kz|) combos)
+#pragma unroll 1
+        for (int e = 0; e < 27; ++e) {
+            const int k = near_slot[e];
+            if (k < 0) continue;
+            const int ax = e % 3, ay = (e / 3) % 3, az = e / 9;
+            double p, gx, gy, gz;
+            m2l_near_small(nm, near_tab, xa, y, z, cluster_of(xa, ax), cluster_of(y, ay), cluster_of(z, az), dx,
+                           p, gx, gy, gz);
+            double* w = wk + (k * 8) * MIR_THREADS;
+            w[0] = p;
+            w[MIR_THREADS] = gx;
+            w[2 * MIR_THREADS] = gy;
+            w[3 * MIR_THREADS] = gz;
+            m2l_near_small(nm, near_tab, xb, y, z, cluster_of(xb, ax), cluster_of(y, ay), cluster_of(z, az), dx,
+                           p, gx, gy, gz);
+            w[4 * MIR_THREADS] = p;
+            w[5 * MIR_THREADS] = gx;
+            w[6 * MIR_THREADS] = gy;
+            w[7 * MIR_THREADS] = gz;
+        }
+        double ap = 0.0, ax_ = 0.0, ay_ = 0.0, az_ = 0.0;
+        double bp = 0.0, bx_ = 0.0, by_ = 0.0, bz_ = 0.0;
+#pragma unroll 1
+        for (int cz = 0; cz < NC; ++cz) {
+            const double rz = mul(sub(tz, add((double)(2 * cz - 8), 1.0)), dx);
+            const int azr = fold(z - 2 * cz + 7);
+#pragma unroll 1
+            for (int cy = 0; cy < NC; ++cy) {
+                const double ry = mul(sub(ty, add((double)(2 * cy - 8), 1.0)), dx);
+                const int ayr = fold(y - 2 * cy + 7);
+                const double* row = tab + (azr * TAB_N + ayr) * MIR_PITCH;
+                const double4* crow = cl + (cz * NC + cy) * NC;
+                if (!__any_sync(0xffffffffu, signbit_d(row[0]))) {
+#pragma unroll
+                    for (int cx = 0; cx < NC; ++cx) {
+                        const int a = axv[cx];
+                        const double inv = row[a], inv3 = row[15 + a], i5 = row[30 + a];
+                        mir_far<ORDER>(crow[cx], inv, inv3, i5, rxv[cx], ry, rz, ap, ax_, ay_, az_);
+                        mir_far<ORDER>(crow[NC - 1 - cx], inv, inv3, i5, -rxv[cx], ry, rz, bp, bx_, by_, bz_);
+                    }
+                } else {
+                    const int rowslot = (azr * 3 + ayr) * 3;
+#pragma unroll
+                    for (int cx = 0; cx < NC; ++cx) {
+                        const int a = axv[cx];
+                        const double inv = row[a], inv3 = row[15 + a], i5 = row[30 + a];
+                        if (!signbit_d(inv)) {
+                            mir_far<ORDER>(crow[cx], inv, inv3, i5, rxv[cx], ry, rz, ap, ax_, ay_, az_);
+                            mir_far<ORDER>(crow[NC - 1 - cx], inv, inv3, i5, -rxv[cx], ry, rz, bp, bx_, by_, bz_);
+                        } else {
+                            const double* w = wk + (near_slot[rowslot + a] * 8) * MIR_THREADS;
+                            ap = add(ap, w[0]);
+                            ax_ = add(ax_, w[MIR_THREADS]);
+                            ay_ = add(ay_, w[2 * MIR_THREADS]);
+                            az_ = add(az_, w[3 * MIR_THREADS]);
+                            bp = add(bp, w[4 * MIR_THREADS]);
+                            bx_ = add(bx_, w[5 * MIR_THREADS]);
+                            by_ = add(by_, w[6 * MIR_THREADS]);
+                            bz_ = add(bz_, w[7 * MIR_THREADS]);
+                        }
+                    }
+                }
+            }
+        }
+        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy;
+        o[xa] = ap;
+        o[ov.comp_stride + xa] = ax_;
+        o[2 * ov.comp_stride + xa] = ay_;
+        o[3 * ov.comp_stride + xa] = az_;
+        o[xb] = bp;
+        o[ov.comp_stride + xb] = bx_;
+        o[2 * ov.comp_stride + xb] = by_;
+        o[3 * ov.comp_stride + xb] = bz_;
+    }
+}
+
 static int g_sm_count = 0;
 int sm_count() {
     if (g_sm_count == 0) {
@@ -701,7 +894,8 @@ int64_t sg_m2l_workspace_bytes(int64_t nleaves) {
     m2l_shape(nleaves > 0 ? nleaves : 1, &threads, &grid);
     const int64_t sms = sm_count();
     if (grid < sms && nleaves > sms) grid = sms;
-    return grid * M2L_WORK_PER_CTA * (int64_t)sizeof(double);
+    const int64_t per = M2L_WORK_PER_CTA > MIR_WORK_PER_CTA ? M2L_WORK_PER_CTA : MIR_WORK_PER_CTA;
+    return (grid > sms ? grid : sms) * per * (int64_t)sizeof(double);
 }
 
 int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
@@ -774,7 +968,19 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     // bits do not depend on the launch shape.
     const int64_t sms = sm_count();
     const int64_t rem = nleaves % sms;
-    if (nleaves > sms && rem > 0 && 2 * rem <= sms) {
+    if (precision == SG_PREC_FMA && small_near && i0 <= 0 && i1 >= 512 && nleaves >= sms) {
+        // FMA mode, full rounds: mirror-paired kernel (one CTA per SM)
+        const int64_t full = nleaves - (2 * rem <= sms ? rem : 0);
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MIR_SMEM);
+            sg_count_launch(1);
+            kern<<<(unsigned)sms, MIR_THREADS, MIR_SMEM, (cudaStream_t)stream>>>(mv, cv, leaves, full, dx, rad2,
+                                                                                 eps2, ov, workspace);
+        };
+        if (order == 1) go(m2l_mirror_kernel<1>);
+        else go(m2l_mirror_kernel<0>);
+        if (full < nleaves) launch_range(full, nleaves - full);
+    } else if (nleaves > sms && rem > 0 && 2 * rem <= sms) {
         launch_range(0, nleaves - rem);
         launch_range(nleaves - rem, rem);
     } else {
