@@ -184,7 +184,7 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
 
 __global__ void __launch_bounds__(P2P_THREADS, 2)
 p2p_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, double dx, double rad2,
-           double eps2, int halo, FieldView ov, double* __restrict__ out_base) {
+           double eps2, int halo, FieldView ov) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int S = NIN + 2 * halo;
     const int pitch = p2p_pitch(S);
@@ -868,7 +868,7 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     sg_count_launch(1);
     p2p_kernel<<<(unsigned)grid, P2P_THREADS, smem, (cudaStream_t)stream>>>(
-        mv, leaves, nleaves, dx, rad2, eps2, halo, ov, out);
+        mv, leaves, nleaves, dx, rad2, eps2, halo, ov);
     return sg_check_launch("sg_p2p");
 }
 

@@ -398,10 +398,10 @@ class LocalSlabs:
 
 def run_steps(state: dict, level: int, steps: int, *, hydro: HydroConfig | None = None,
               gravity: GravityConfig | None = None, gravity_per_step: int = 6, slab: Slab | None = None,
-              group=None, check_every_step: bool = True) -> tuple[dict, list]:
+              group=None, check_every_step: bool = True, precision: str = "exact") -> tuple[dict, list]:
     """Public end-to-end entry: host arrays in, ``steps`` reference timesteps on
     the device, host arrays out (plus the per-step dt values)."""
-    st = UnigridState(level, hydro, gravity, slab=slab, group=group)
+    st = UnigridState(level, hydro, gravity, slab=slab, group=group, precision=precision)
     st.load(state)
     dts = []
     for s in range(steps):

@@ -18,7 +18,7 @@ import torch
 from . import batched as B
 from .kernels import FluxField, HydroConfig, KernelError, QuadratureField, _raise_flux_error, _to_dev, reconstruct
 
-__all__ = ["legacy_reconstruct", "legacy_flux", "decode_legacy_flux_error"]
+__all__ = ["legacy_reconstruct", "legacy_flux", "decode_legacy_flux_error", "KernelError"]
 
 
 def legacy_reconstruct(sub, cfg: HydroConfig, backend=None) -> QuadratureField:
@@ -47,5 +47,3 @@ def legacy_flux(sub, q: QuadratureField, cfg: HydroConfig, backend=None) -> Flux
         _raise_flux_error(sub, code, cell)
     return FluxField(FX.cpu().numpy(), FY.cpu().numpy(), FZ.cpu().numpy(), float(smax.item()))
 
-
-assert KernelError  # re-exported error type of the legacy entry points

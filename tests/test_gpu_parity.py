@@ -447,3 +447,19 @@ def test_level5_full_step_conserves():
     assert np.isfinite(out["phi"]).all() and np.isfinite(out["gz"]).all()
     del u
     torch.cuda.empty_cache()
+
+
+def test_run_steps_public_entry(manifest):
+    """grid.run_steps (host arrays in and out) reproduces the config-5 L=2
+    reference run: per-step dt and final state."""
+    m = manifest["cfg5_L2"]
+    st = scenarios.config5_state(2)
+    if digest(np.stack([st[k] for k in octree.HYDRO_FIELDS])) != m["input_digest"]:
+        pytest.skip("config-5 generator differs on this host")
+    out, dts = G.run_steps(st, 2, 10, hydro=K.HydroConfig(gamma=1.4),
+                           gravity=K.GravityConfig(theta=0.34, eps=0.5, expansion_order=1))
+    assert [d.hex() for d in dts] == m["dts"]
+    for k in octree.HYDRO_FIELDS:
+        assert digest(out[k]) == m["final_field_digests"][k], k
+    g = np.stack([out[k] for k in ("phi", "gx", "gy", "gz")])
+    assert digest(g) == m["gravity_digests"]["9"]
