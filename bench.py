@@ -236,7 +236,7 @@ def fp64_peak(torch) -> dict:
 def per_config_rates(torch, peaks: dict) -> dict:
     """Per-kernel device rates on BASELINE configs 1-4 (SURVEY.md 8(d)
     restatements), median of 5 CUDA-event timed launches after a warm-up;
-    inputs resident.  FP64 fractions are against the measured DADD issue peak
+    inputs resident, host enqueue hidden.  FP64 fractions are against the measured DADD issue peak
     (the attainable roof without FMA contraction); reconstruct's against HBM."""
     import statistics as stats
 
@@ -250,6 +250,7 @@ def per_config_rates(torch, peaks: dict) -> dict:
         ts = []
         for _ in range(reps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(200000)  # GPU busy while the host enqueues: device time only
             a.record()
             fn()
             b.record()
@@ -265,7 +266,8 @@ def per_config_rates(torch, peaks: dict) -> dict:
         pass
     out = {}
     g1 = GravityConfig(theta=0.34, eps=0.5, expansion_order=1)
-    # config 1: one 24^3 neighbourhood (latency: one CTA)
+    # config 1: one 24^3 neighbourhood (M2L latency mode: 144 term CTAs +
+    # the ordered per-target reduction)
     cube = torch.from_numpy(scenarios.config1_cube(0)).cuda()
     cl = torch.empty((12, 12, 12, 4), dtype=torch.float64, device="cuda")
     res = torch.empty((4, 8, 8, 8), dtype=torch.float64, device="cuda")

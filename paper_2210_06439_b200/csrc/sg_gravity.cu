@@ -771,6 +771,181 @@ m2l_mirror_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leav
     }
 }
 
+// ---------------------------------------------------------------------------
+// Latency mode for tiny batches ("generate terms in
+// parallel across CTAs, then accumulate serially per target"), used when one
+// leaf per persistent CTA would leave the GPU idle (config 1, the drop-in
+// per-subgrid calls).  m2l_terms_kernel evaluates every (target, cluster)
+// term of compiled.py:399-442 -- the selected far or near value, same
+// expression trees -- with one CTA per (leaf, cz, cy) row of 12 clusters;
+// m2l_reduce_kernel then sums each target's 1728 terms in the reference's
+// (cz, cy, cx) order from shared memory.  Bit-identical to m2l_kernel: the
+// sums see the same terms in the same order (a term stored as -0.0 adds
+// exactly like the reference's, whose accumulators are never -0.0).
+// Terms layout: [leaf][comp 4][cluster 1728][target 512] doubles (coalesced
+// stores; the reduction reads 64-byte runs of 8 targets).
+// ---------------------------------------------------------------------------
+constexpr int NCL = NC * NC * NC;                                           // 1728
+constexpr int64_t LAT_MAX_LEAVES = 4;  // 28 MB of terms per leaf: keep them L2-resident
+constexpr int64_t LAT_TERMS_PER_LEAF = (int64_t)NCL * 4 * M2L_THREADS;      // doubles
+constexpr int LAT_PITCH = 48;                                               // [inv|inv3|inv5] x 16
+constexpr size_t LAT_SMEM = sizeof(double) * 64 * LAT_PITCH + sizeof(double2) * NEAR_R * NEAR_R * NEAR_R +
+                            sizeof(double4) * NC + sizeof(double) * NBW * NBW * NBW;
+constexpr int RED_T = 8;               // targets per reduce CTA (2 CTAs per SM)
+constexpr int RED_PITCH = RED_T;       // smem [cluster][target]: a row of 8 doubles
+constexpr size_t RED_SMEM = sizeof(double) * NCL * RED_PITCH;
+
+template <int ORDER, bool SMALL_NEAR>
+__global__ void __launch_bounds__(M2L_THREADS, 1)
+m2l_terms_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, double dx, double rad2,
+                 double eps2, double* __restrict__ terms) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* tab = reinterpret_cast<double*>(smem_raw);  // rows (z, y): this CTA's (az, ay) pairs
+    double2* near_tab = reinterpret_cast<double2*>(tab + 64 * LAT_PITCH);
+    double4* cl = reinterpret_cast<double4*>(near_tab + NEAR_R * NEAR_R * NEAR_R);
+    double* nm = reinterpret_cast<double*>(cl + NC);
+    const int tid = threadIdx.x;
+    const int64_t b = blockIdx.x / (NC * NC);
+    const int cy = (blockIdx.x / NC) % NC, cz = blockIdx.x % NC;
+    // stage this CTA's row of 12 clusters and (rows that can hold near
+    // clusters: 2 <= c <= 9 on every axis) the near masses asynchronously,
+    // overlapping the geometry below
+    const double* mc = leaf_origin(mv, leaves, b, 8);
+    const bool near_row = SMALL_NEAR && cz >= 2 && cz <= 9 && cy >= 2 && cy <= 9;
+    if (tid < 2 * NC) {
+        int64_t cx0 = cv.off + (tid >> 1), cy0 = cv.off + cy, cz0 = cv.off + cz;
+        if (leaves) {
+            cx0 += 4 * (int64_t)leaves[3 * b];
+            cy0 += 4 * (int64_t)leaves[3 * b + 1];
+            cz0 += 4 * (int64_t)leaves[3 * b + 2];
+        }
+        const double* src =
+            reinterpret_cast<const double*>(cv.base + b * cv.leaf_stride + cz0 * cv.sz + cy0 * cv.sy + cx0) +
+            2 * (tid & 1);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(reinterpret_cast<double*>(cl) + 2 * tid);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+    }
+    if (near_row) {
+        for (int i = tid; i < NBW * NBW * NBW; i += M2L_THREADS) {
+            const int x = i % NBW, y = (i / NBW) % NBW, z = i / (NBW * NBW);
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(nm + i);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                         "l"(mc + (int64_t)(z + NB0) * mv.sz + (int64_t)(y + NB0) * mv.sy + (x + NB0))
+                         : "memory");
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    // geometry for rows az = fold(z - 2cz + 7), ay = fold(y - 2cy + 7), as m2l_kernel's table
+    for (int e = tid; e < 64 * TAB_N; e += M2L_THREADS) {
+        const int ax = e % TAB_N, zy = e / TAB_N;
+        const int az = fold((zy >> 3) - 2 * cz + 7), ay = fold((zy & 7) - 2 * cy + 7);
+        const double rx = mul(add((double)ax, 0.5), dx);
+        const double ry = mul(add((double)ay, 0.5), dx);
+        const double rz = mul(add((double)az, 0.5), dx);
+        const double r2 = add(add(mul(rx, rx), mul(ry, ry)), mul(rz, rz));
+        double* row = tab + zy * LAT_PITCH;
+        if (r2 > rad2) {
+            const double inv = dvd(1.0, dsqrt(add(r2, eps2)));
+            const double inv3 = mul(mul(inv, inv), inv);
+            row[ax] = inv;
+            row[16 + ax] = inv3;
+            row[32 + ax] = mul(mul(inv3, inv), inv);
+        } else {
+            row[ax] = -1.0;
+            row[16 + ax] = 0.0;
+            row[32 + ax] = 0.0;
+        }
+    }
+    for (int e = tid; e < NEAR_R * NEAR_R * NEAR_R; e += M2L_THREADS) {
+        const int ix = e % NEAR_R, iy = (e / NEAR_R) % NEAR_R, iz = e / (NEAR_R * NEAR_R);
+        const double sx = mul((double)ix, dx), sy = mul((double)iy, dx), sz = mul((double)iz, dx);
+        const double r2s = add(add(mul(sx, sx), mul(sy, sy)), mul(sz, sz));
+        if (r2s > 0.0) {
+            const double invs = dvd(1.0, dsqrt(add(r2s, eps2)));
+            near_tab[e] = make_double2(invs, mul(mul(invs, invs), invs));
+        } else {
+            near_tab[e] = make_double2(-1.0, 0.0);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;
+    const double tx = (double)x + 0.5, ty = (double)y + 0.5, tz = (double)z + 0.5;
+    const double rz = mul(sub(tz, add((double)(2 * cz - 8), 1.0)), dx);
+    const double ry = mul(sub(ty, add((double)(2 * cy - 8), 1.0)), dx);
+    const double* row = tab + (z * 8 + y) * LAT_PITCH;
+    double* o = terms + b * LAT_TERMS_PER_LEAF + (int64_t)((cz * NC + cy) * NC) * M2L_THREADS + tid;
+    const int64_t cs = (int64_t)NCL * M2L_THREADS;  // component stride
+#pragma unroll 1
+    for (int cx = 0; cx < NC; ++cx) {
+        const int ax = fold(x - 2 * cx + 7);
+        double p = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+        if (!signbit_d(row[ax])) {
+            const double rx = mul(sub(tx, add((double)(2 * cx - 8), 1.0)), dx);
+            m2l_far<ORDER, false>(row, ax, cl[cx], rx, ry, rz, p, gx, gy, gz);
+        } else if (SMALL_NEAR) {
+            m2l_near_small(nm, near_tab, x, y, z, cx, cy, cz, dx, p, gx, gy, gz);
+        } else {
+            double r[4];
+            m2l_near(mc, mv.sy, mv.sz, near_tab, x, y, z, cx, cy, cz, dx, eps2, r);
+            p = r[0];
+            gx = r[1];
+            gy = r[2];
+            gz = r[3];
+        }
+        double* oc = o + (int64_t)cx * M2L_THREADS;
+        oc[0] = p;
+        oc[cs] = gx;
+        oc[2 * cs] = gy;
+        oc[3 * cs] = gz;
+    }
+}
+
+// one CTA per (leaf, component, 8 targets): 256 threads stage the 8 x 1728
+// terms in shared memory with cp.async (two halves, so the chains start on
+// the first while the second lands), 8 threads run the ordered chains
+__global__ void __launch_bounds__(256)
+m2l_reduce_kernel(const double* __restrict__ terms, const int32_t* __restrict__ leaves, int i0, int i1,
+                  FieldView ov) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* buf = reinterpret_cast<double*>(smem_raw);
+    constexpr int GROUPS = M2L_THREADS / RED_T;
+    const int tg = blockIdx.x % GROUPS;
+    const int comp = (blockIdx.x / GROUPS) % 4;
+    const int64_t b = blockIdx.x / (GROUPS * 4);
+    const double* src = terms + b * LAT_TERMS_PER_LEAF + (int64_t)comp * NCL * M2L_THREADS + tg * RED_T;
+    constexpr int HALF = NCL / 2;  // clusters per stage; 4 16-byte chunks per cluster
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+        for (int i = threadIdx.x; i < HALF * 4; i += 256) {
+            const int c = h * HALF + (i >> 2), r = 2 * (i & 3);
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(buf + c * RED_PITCH + r);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
+                         "l"(src + (int64_t)c * M2L_THREADS + r)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    double acc = 0.0;
+    const double* row = buf + threadIdx.x;
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < RED_T) {
+#pragma unroll 16
+        for (int c = 0; c < HALF; ++c) acc = add(acc, row[c * RED_PITCH]);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x >= RED_T) return;
+#pragma unroll 16
+    for (int c = HALF; c < NCL; ++c) acc = add(acc, row[c * RED_PITCH]);
+    const int t = tg * RED_T + threadIdx.x;
+    if (t < i0 || t >= i1) return;
+    const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+    double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy + x;
+    o[comp * ov.comp_stride] = acc;
+}
+
 static int g_sm_count = 0;
 int sm_count() {
     if (g_sm_count == 0) {
@@ -895,7 +1070,12 @@ int64_t sg_m2l_workspace_bytes(int64_t nleaves) {
     const int64_t sms = sm_count();
     if (grid < sms && nleaves > sms) grid = sms;
     const int64_t per = M2L_WORK_PER_CTA > MIR_WORK_PER_CTA ? M2L_WORK_PER_CTA : MIR_WORK_PER_CTA;
-    return (grid > sms ? grid : sms) * per * (int64_t)sizeof(double);
+    int64_t bytes = (grid > sms ? grid : sms) * per * (int64_t)sizeof(double);
+    if (nleaves <= LAT_MAX_LEAVES) {  // latency mode stores every (target, cluster) term
+        const int64_t lat = nleaves * LAT_TERMS_PER_LEAF * (int64_t)sizeof(double);
+        if (lat > bytes) bytes = lat;
+    }
+    return bytes;
 }
 
 int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
@@ -968,7 +1148,27 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     // bits do not depend on the launch shape.
     const int64_t sms = sm_count();
     const int64_t rem = nleaves % sms;
-    if (precision == SG_PREC_FMA && small_near && i0 <= 0 && i1 >= 512 && nleaves >= sms) {
+    if (nleaves <= LAT_MAX_LEAVES) {
+        // latency mode (small batches, e.g. one subgrid): terms over
+        // nleaves x 12 CTAs, then the ordered per-target reduction
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LAT_SMEM);
+            sg_count_launch(1);
+            kern<<<(unsigned)(nleaves * NC * NC), M2L_THREADS, LAT_SMEM, (cudaStream_t)stream>>>(mv, cv, leaves, dx,
+                                                                                                rad2, eps2, workspace);
+        };
+        if (order == 1) {
+            if (small_near) go(m2l_terms_kernel<1, true>);
+            else go(m2l_terms_kernel<1, false>);
+        } else {
+            if (small_near) go(m2l_terms_kernel<0, true>);
+            else go(m2l_terms_kernel<0, false>);
+        }
+        cudaFuncSetAttribute(m2l_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RED_SMEM);
+        sg_count_launch(1);
+        m2l_reduce_kernel<<<(unsigned)(nleaves * 4 * (M2L_THREADS / RED_T)), 256, RED_SMEM, (cudaStream_t)stream>>>(
+            workspace, leaves, i0, i1, ov);
+    } else if (precision == SG_PREC_FMA && small_near && i0 <= 0 && i1 >= 512 && nleaves >= sms) {
         // FMA mode, full rounds: mirror-paired kernel (one CTA per SM)
         const int64_t full = nleaves - (2 * rem <= sms ? rem : 0);
         auto go = [&](auto kern) {

@@ -400,7 +400,7 @@ def test_batched_kernels_on_permuted_leaf_subsets(manifest):
     B.cluster_aggregate(mass, 1.0 / 64, cl)
     rad2, eps2 = K.gravity_params(1.0 / 64, K.GravityConfig())
     allc = [(x, y, z) for z in range(8) for y in range(8) for x in range(8)]
-    for count in (3, 40, 200):
+    for count in (1, 3, 12, 13, 40, 200):
         pick = [allc[i] for i in rng.permutation(512)[:count]]
         leaves = torch.tensor(pick, dtype=torch.int32, device="cuda")
         out = torch.zeros((4, n, n, n), dtype=torch.float64, device="cuda")
@@ -463,3 +463,42 @@ def test_run_steps_public_entry(manifest):
         assert digest(out[k]) == m["final_field_digests"][k], k
     g = np.stack([out[k] for k in ("phi", "gx", "gy", "gz")])
     assert digest(g) == m["gravity_digests"]["9"]
+
+
+@pytest.mark.parametrize("theta,order", [(0.34, 0), (0.5, 1), (0.2, 1), (0.2, 0)])
+def test_m2l_latency_mode_equals_persistent(theta, order):
+    """Batches of <= 4 subgrids take the two-kernel latency mode (terms over
+    144 CTAs per leaf + ordered reduction); every leaf matches the persistent
+    kernel's bits, near-field regimes (theta 0.2: generic near path) and
+    both expansion orders included."""
+    rng = np.random.default_rng(7)
+    n, level = 32, 2
+    dx = 1.0 / n
+    mv = View(n, n, n, 8)
+    mass = torch.zeros(mv.padded_shape, dtype=torch.float64, device="cuda")
+    mass[8:8 + n, 8:8 + n, 8:8 + n] = dev(rng.random((n, n, n)) * dx ** 3)
+    B.fill_periodic(mass, 1, mv, 7)
+    z_, y_, x_ = mv.padded_shape
+    cl = torch.empty((z_ // 2, y_ // 2, x_ // 2, 4), dtype=torch.float64, device="cuda")
+    B.cluster_aggregate(mass, dx, cl)
+    rad2, eps2 = K.gravity_params(dx, K.GravityConfig(theta=theta, eps=0.5))
+    allc = [(x, y, z) for z in range(4) for y in range(4) for x in range(4)]
+    full = torch.zeros((4, n, n, n), dtype=torch.float64, device="cuda")
+    leaves = torch.tensor(allc, dtype=torch.int32, device="cuda")
+    B.m2l(mass, mv, cl, 0, leaves, 64, dx, rad2, eps2, order, full, View(n, n, n, 0))
+    want = full.cpu().numpy()
+    for count in (1, 3, 4):
+        pick = [allc[i] for i in rng.permutation(64)[:count]]
+        out = torch.full((4, n, n, n), np.nan, dtype=torch.float64, device="cuda")
+        B.m2l(mass, mv, cl, 0, torch.tensor(pick, dtype=torch.int32, device="cuda"), count, dx, rad2, eps2, order,
+              out, View(n, n, n, 0))
+        o = out.cpu().numpy()
+        for (cx, cy, cz) in pick:
+            s = np.s_[:, cz * 8:cz * 8 + 8, cy * 8:cy * 8 + 8, cx * 8:cx * 8 + 8]
+            assert bitwise(o[s], want[s]), (count, cx, cy, cz)
+    # a sub-range of targets writes only those cells
+    out = torch.full((4, n, n, n), 7.0, dtype=torch.float64, device="cuda")
+    B.m2l(mass, mv, cl, 0, leaves[:1], 1, dx, rad2, eps2, order, out, View(n, n, n, 0), 100, 333)
+    blk = out[:, :8, :8, :8].reshape(4, 512).cpu().numpy()
+    assert bitwise(blk[:, 100:333], want[:, :8, :8, :8].reshape(4, 512)[:, 100:333])
+    assert (blk[:, :100] == 7.0).all() and (blk[:, 333:] == 7.0).all()
