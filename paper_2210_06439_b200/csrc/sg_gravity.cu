@@ -478,21 +478,26 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
                 cy0 += 4 * (int64_t)leaves[3 * b + 1];
                 cz0 += 4 * (int64_t)leaves[3 * b + 2];
             }
+            // cp.async: every thread's loads in flight at once (no register hop)
             const double4* src = cv.base + b * cv.leaf_stride + cz0 * cv.sz + cy0 * cv.sy + cx0;
-            for (int i = tid; i < NC * NC * NC; i += nt) {
-                const int cx = i % NC, cy = (i / NC) % NC, cz = i / (NC * NC);
-                const double2* s2 = reinterpret_cast<const double2*>(src + cz * cv.sz + cy * cv.sy + cx);
-                const double2 a = __ldg(s2), c2 = __ldg(s2 + 1);
-                cl[i] = make_double4(a.x, a.y, c2.x, c2.y);
+            for (int i = tid; i < 2 * NC * NC * NC; i += nt) {
+                const int q = i >> 1, cx = q % NC, cy = (q / NC) % NC, cz = q / (NC * NC);
+                const double* s2 = reinterpret_cast<const double*>(src + cz * cv.sz + cy * cv.sy + cx) + 2 * (i & 1);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(reinterpret_cast<double*>(cl) + 2 * i);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(s2) : "memory");
             }
         }
         const double* mc = leaf_origin(mv, leaves, b, 8);
         if (SMALL_NEAR) {  // stage the near-field masses
             for (int i = tid; i < NBW * NBW * NBW; i += nt) {
                 const int cx = i % NBW, cy = (i / NBW) % NBW, cz = i / (NBW * NBW);
-                nm[i] = __ldg(mc + (int64_t)(cz + NB0) * mv.sz + (int64_t)(cy + NB0) * mv.sy + (cx + NB0));
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(nm + i);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                             "l"(mc + (int64_t)(cz + NB0) * mv.sz + (int64_t)(cy + NB0) * mv.sy + (cx + NB0))
+                             : "memory");
             }
         }
+        asm volatile("cp.async.commit_group;\n" "cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
         if (SMALL_NEAR) {
             // every target has its near clusters at the same (|kx|,|ky|,|kz|)
