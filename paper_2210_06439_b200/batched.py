@@ -9,6 +9,7 @@ interior dims, the pad and the leaf stride (0 for one global field).
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import torch
@@ -87,16 +88,21 @@ def p2p(mass, mv: View, leaves, nleaves: int, dx: float, rad2: float, eps2: floa
 
 
 _WORKSPACE: dict = {}
+_WORKSPACE_LOCK = threading.Lock()
 
 
 def m2l_workspace(nleaves: int, device=None) -> torch.Tensor:
-    """Cached per-device scratch for sg_m2l (grows on demand)."""
+    """Cached scratch for sg_m2l, one per (device, stream): callers on
+    different streams (e.g. pool threads, SURVEY.md 8(b) re-entrancy) never
+    share one; reuse on the same stream is stream-ordered.  Grows on demand."""
     need = int(_lib.load().sg_m2l_workspace_bytes(nleaves))
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    ws = _WORKSPACE.get(dev)
-    if ws is None or ws.numel() * 8 < need:
-        ws = torch.empty((need + 7) // 8, dtype=torch.float64, device=dev)
-        _WORKSPACE[dev] = ws
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    with _WORKSPACE_LOCK:
+        ws = _WORKSPACE.get(key)
+        if ws is None or ws.numel() * 8 < need:
+            ws = torch.empty((need + 7) // 8, dtype=torch.float64, device=dev)
+            _WORKSPACE[key] = ws
     return ws
 
 

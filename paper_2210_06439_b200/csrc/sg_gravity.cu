@@ -16,6 +16,8 @@
 // never -0.0, so skipping x + 0.0 is exact.
 #include <cmath>
 
+#include <atomic>
+
 #include "sg_common.cuh"
 #include "../../include/sg.h"
 
@@ -951,15 +953,19 @@ m2l_reduce_kernel(const double* __restrict__ terms, const int32_t* __restrict__ 
     o[comp * ov.comp_stride] = acc;
 }
 
-static int g_sm_count = 0;
+// SM count of the current device, cached per device (atomic: re-entrant)
+static std::atomic<int> g_sm_count[64] = {};
 int sm_count() {
-    if (g_sm_count == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
-        if (g_sm_count <= 0) g_sm_count = 148;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int n = g_sm_count[dev].load(std::memory_order_relaxed);
+    if (n == 0) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+        g_sm_count[dev].store(n, std::memory_order_relaxed);
     }
-    return g_sm_count;
+    return n;
 }
 
 }  // namespace sg

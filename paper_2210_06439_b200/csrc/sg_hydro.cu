@@ -14,6 +14,9 @@
 // HBM-bound (Q is 1.04 MB per subgrid).  Parallelism comes only from
 // independent outputs (cells, faces, subgrids); every per-output chain keeps
 // the reference's sequential order.
+#include <atomic>
+#include <mutex>
+
 #include "sg_common.cuh"
 #include "../../include/sg.h"
 
@@ -27,9 +30,12 @@ __constant__ int c_dminus[3][9];
 // geometry.py:59-61
 __constant__ double c_simpson[9];
 
-// __constant__ memory is per device: upload the tables once per device
+// __constant__ memory is per device: upload the tables once per device.
+// Re-entrant (concurrent callers on their own streams):
+// the flag is atomic and the first upload per device runs under a mutex.
 constexpr int SG_MAX_DEVICES = 64;
-static bool g_tables_ready[SG_MAX_DEVICES] = {};
+static std::atomic<bool> g_tables_ready[SG_MAX_DEVICES] = {};
+static std::mutex g_tables_mu;
 
 static int host_dir_index(int dz, int dy, int dx) {
     int idx = (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
@@ -42,7 +48,9 @@ static int init_tables() {
         sg_set_error("hydro constant tables: no current CUDA device");
         return SG_ECUDA;
     }
-    if (g_tables_ready[dev]) return SG_OK;
+    if (g_tables_ready[dev].load(std::memory_order_acquire)) return SG_OK;
+    std::lock_guard<std::mutex> lock(g_tables_mu);
+    if (g_tables_ready[dev].load(std::memory_order_relaxed)) return SG_OK;
     double dirs[NDIR][3];
     int d = 0;
     for (int dz = -1; dz <= 1; ++dz)
@@ -76,7 +84,7 @@ static int init_tables() {
         sg_set_error("hydro constant tables: %s", cudaGetErrorString(cudaGetLastError()));
         return SG_ECUDA;
     }
-    g_tables_ready[dev] = true;
+    g_tables_ready[dev].store(true, std::memory_order_release);
     return SG_OK;
 }
 

@@ -115,6 +115,50 @@ def test_dropin_multipole_prepare_chunks():
     assert bitwise(got, g["m2l_t34_o1"][3])
 
 
+
+def test_dropin_concurrent_callers_on_own_streams():
+    """SURVEY.md 8(b) re-entrancy: pool threads call the entry points
+    concurrently, each on its own CUDA stream, and a leaf's run(i0, i1)
+    chunks are split across threads/streams (driver.py:135-139) -- every leaf
+    still gets its golden bits."""
+    import threading
+
+    g = load_npz("gravity_tree.npz")
+    cfg_m = K.GravityConfig(theta=0.34, expansion_order=1)
+    cfg_p = K.GravityConfig(theta=0.34)
+    mono_tree, multi_tree = _tree_from_mass(g["mass"]), _tree_from_mass(g["mass"])
+    runs = [K.multipole_prepare(multi_tree.leaves[i], octree.neighborhood27(multi_tree, i), cfg_m, "scalar")
+            for i in range(8)]
+    errors = []
+
+    def worker(tid):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                for rep in range(3):
+                    for i in range(8):
+                        if (i + rep) % 4 == tid:
+                            K.monopole_kernel(mono_tree.leaves[i], octree.neighborhood27(mono_tree, i), cfg_p)
+                # chunk c of every leaf on thread c % 4
+                for i in range(8):
+                    for c, (a, b) in enumerate(((0, 128), (128, 256), (256, 384), (384, 512))):
+                        if c == tid:
+                            runs[i](a, b)
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for i in range(8):
+        got_p = np.stack([mono_tree.leaves[i].interior(n) for n in ("phi", "gx", "gy", "gz")])
+        got_m = np.stack([multi_tree.leaves[i].interior(n) for n in ("phi", "gx", "gy", "gz")])
+        assert bitwise(got_p, g["p2p_t34_o0"][i]), i
+        assert bitwise(got_m, g["m2l_t34_o1"][i]), i
+
+
 # -- batched configs 2-4 --------------------------------------------------------
 
 def _batched_gravity(level, mass, kind, theta, order):
