@@ -34,16 +34,18 @@ def decode_legacy_flux_error(err: int) -> tuple[int, int]:
 
 def legacy_flux(sub, q: QuadratureField, cfg: HydroConfig, backend=None) -> FluxField:
     """reference legacy.py:157-167 (``backend`` accepted and ignored)."""
-    dQ = _to_dev(q.values)
+    dQ = q.device_values() if isinstance(q, QuadratureField) else None
+    if dQ is None:
+        dQ = _to_dev(q.values)
     dev = dQ.device
     FX = torch.empty((5, 8, 8, 9), dtype=torch.float64, device=dev)
     FY = torch.empty((5, 8, 9, 8), dtype=torch.float64, device=dev)
     FZ = torch.empty((5, 9, 8, 8), dtype=torch.float64, device=dev)
-    smax = torch.empty(1, dtype=torch.float64, device=dev)
-    err = torch.empty(1, dtype=torch.int32, device=dev)
-    B.flux_legacy(dQ, 1, cfg.gamma, FX, FY, FZ, smax, err)
-    code, cell = decode_legacy_flux_error(int(err.cpu().numpy().view(np.uint32)[0]))
+    status = torch.empty(2, dtype=torch.float64, device=dev)  # [smax, err word]: one readback
+    B.flux_legacy(dQ, 1, cfg.gamma, FX, FY, FZ, status[0:1], status[1:2].view(torch.int32)[0:1])
+    st = status.cpu().numpy()
+    code, cell = decode_legacy_flux_error(int(st[1:2].view(np.uint32)[0]))
     if code != 0:
         _raise_flux_error(sub, code, cell)
-    return FluxField(FX.cpu().numpy(), FY.cpu().numpy(), FZ.cpu().numpy(), float(smax.item()))
+    return FluxField(max_speed=float(st[0]), device_values=(FX, FY, FZ))
 

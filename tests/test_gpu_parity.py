@@ -262,6 +262,34 @@ def test_dropin_hydro_random_blocks():
         i += 1
 
 
+def test_dropin_hydro_chain_stays_on_device():
+    """reconstruct -> flux -> hydro_update without touching the host arrays
+    keeps Q and the fluxes on the device; the results (and the lazily copied
+    host arrays) equal the goldens, and an edit of q.values is honoured."""
+    g = load_npz("hydro_random.npz")
+    cfg = K.HydroConfig()
+    for i in range(2):
+        sub = _sub_from_block(g[f"U{i}"])
+        q = K.reconstruct(sub, cfg)
+        assert q.device_values() is not None
+        fl = K.flux(sub, q, cfg)
+        assert all(fl.device_values(k) is not None for k in range(3))
+        meta = g[f"flux_meta{i}"]
+        assert fl.max_speed == meta[0]
+        want = g[f"Uupd{i}"]
+        if not ((want[0] > 0).all() and (want[4] > 0).all()):
+            continue
+        K.hydro_update(sub, fl, meta[3], cfg)
+        assert bitwise(np.stack([sub.interior(n) for n in octree.HYDRO_FIELDS]), want), i
+        assert bitwise(fl.fx, g[f"FX{i}"]) and bitwise(fl.fy, g[f"FY{i}"]) and bitwise(fl.fz, g[f"FZ{i}"])
+        assert digest(q.values) == str(g[f"Qdigest{i}"]) and q.device_values() is None
+    sub = _sub_from_block(g["U0"])
+    q = K.reconstruct(sub, cfg)
+    q.values[0, 0, 5, 5, 5] = -1.0  # host edit: flux must see it
+    with pytest.raises(K.KernelError, match="density"):
+        K.flux(sub, q, cfg)
+
+
 def test_flux_error_first_in_loop_order():
     g = load_npz("hydro_random.npz")
     cfg = K.HydroConfig()

@@ -181,3 +181,26 @@ class TestStatusWords:
         assert K.decode_flux_error(0xFFFFFFFF) == (0, -1)
         key = 12345
         assert K.decode_flux_error((key << 12) | (2 << 10) | 987) == (2, 987)
+
+
+def test_source_cube_is_periodic_window_of_global_field():
+    """octree.source_cube (reference octree.py:186-214) == the periodic
+    (8+2h)^3 window of the global field around the leaf, every halo 0..8."""
+    import numpy as np
+
+    from paper_2210_06439_b200 import octree
+
+    tree = octree.build_unigrid(2)
+    rng = np.random.default_rng(5)
+    F = rng.random((32, 32, 32))
+    octree.set_global_field(tree, "mass", F)
+    for lid in (0, 9, 63):
+        cx, cy, cz = tree.leaves[lid].coord
+        nb = octree.neighborhood27(tree, lid)
+        for h in range(0, 9):
+            r = np.arange(-h, 8 + h)
+            want = F[np.ix_((cz * 8 + r) % 32, (cy * 8 + r) % 32, (cx * 8 + r) % 32)]
+            assert np.array_equal(octree.source_cube(nb, "mass", h), want), (lid, h)
+    import pytest
+    with pytest.raises(ValueError):
+        octree.source_cube(nb, "mass", 9)
