@@ -24,6 +24,12 @@
  *      batched path : one global padded field, leaf_stride 0, leaf coords;
  *      drop-in path : a stack of per-subgrid blocks, leaf_stride = block
  *                     volume * ncomp, leaves == NULL.
+ *  - Validation (before any CUDA call): NULL required pointers, negative or
+ *    zero interior dims, negative pads/strides, bad halo/order/precision ->
+ *    SG_EINVAL with the argument named in sg_last_error().  An empty batch
+ *    (nleaves <= 0) is a no-op.  Preconditions the library cannot check
+ *    without reading device memory: leaf coordinates lie inside the view
+ *    (0 <= 8*c < interior dim per axis) and buffers have the documented sizes.
  *  - Arithmetic is FP64, IEEE round-to-nearest, no FMA contraction, the
  *    reference's association and accumulation order: bit-identical results.
  */

@@ -76,3 +76,11 @@ __device__ __forceinline__ bool signbit_d(double v) {
 void sg_set_error(const char* fmt, ...);
 void sg_count_launch(int n);
 int sg_check_launch(const char* what);
+int sg_check_view(const char* fn, const char* name, const void* base, int64_t nx, int64_t ny, int64_t nz,
+                  int32_t pad, int64_t leaf_stride);
+int sg_check_ptr(const char* fn, const char* name, const void* p);
+#define SG_TRY(expr)          \
+    do {                      \
+        int sg_rc_ = (expr);  \
+        if (sg_rc_) return sg_rc_; \
+    } while (0)

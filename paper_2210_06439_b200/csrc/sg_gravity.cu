@@ -982,6 +982,8 @@ int sg_cluster_aggregate(const double* mass, int64_t mnx, int64_t mny, int64_t m
         return SG_EINVAL;
     }
     if (nleaf < 1) nleaf = 1;
+    SG_TRY(sg_check_view("sg_cluster_aggregate", "mass", mass, mnx, mny, mnz, 0, 0));
+    SG_TRY(sg_check_ptr("sg_cluster_aggregate", "clusters", clusters));
     const int64_t ncx = mnx / 2, ncy = mny / 2, ncz = mnz / 2;
     const int64_t total = ncx * ncy * ncz * nleaf;
     if (total == 0) return SG_OK;
@@ -1001,6 +1003,12 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
         return SG_EINVAL;
     }
     if (nleaves <= 0) return SG_OK;
+    SG_TRY(sg_check_view("sg_p2p", "mass", mass, nx, ny, nz, pad, leaf_stride));
+    SG_TRY(sg_check_view("sg_p2p", "out", out, onx, ony, onz, 0, out_leaf_stride));
+    if (precision != SG_PREC_EXACT && precision != SG_PREC_FMA) {
+        sg_set_error("sg_p2p: unknown precision mode %d", precision);
+        return SG_EINVAL;
+    }
     FieldView mv = make_view(mass, nx, ny, nz, pad, leaf_stride);
     FieldView ov = make_view(out, onx, ony, onz, 0, out_leaf_stride);
     const int S = NIN + 2 * halo;
@@ -1107,6 +1115,13 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
         return SG_EINVAL;
     }
     if (nleaves <= 0 || i1 <= i0) return SG_OK;
+    SG_TRY(sg_check_view("sg_m2l", "mass", mass, nx, ny, nz, pad, leaf_stride));
+    SG_TRY(sg_check_ptr("sg_m2l", "clusters", clusters));
+    SG_TRY(sg_check_view("sg_m2l", "out", out, onx, ony, onz, 0, out_leaf_stride));
+    if (cluster_leaf_stride < 0) {
+        sg_set_error("sg_m2l: negative cluster leaf stride");
+        return SG_EINVAL;
+    }
     if (!workspace || workspace_bytes < sg_m2l_workspace_bytes(nleaves)) {
         sg_set_error("sg_m2l: workspace of %lld bytes required (got %lld)",
                      (long long)sg_m2l_workspace_bytes(nleaves), (long long)workspace_bytes);

@@ -21,6 +21,29 @@ static unsigned long long g_launches = 0;  // kernels launched by this library
 
 void sg_count_launch(int n) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
 
+// argument validation shared by the entry points (runs before any CUDA call)
+int sg_check_view(const char* fn, const char* name, const void* base, int64_t nx, int64_t ny, int64_t nz,
+                  int32_t pad, int64_t leaf_stride) {
+    if (!base) {
+        sg_set_error("%s: %s is NULL", fn, name);
+        return SG_EINVAL;
+    }
+    if (nx <= 0 || ny <= 0 || nz <= 0 || pad < 0 || leaf_stride < 0) {
+        sg_set_error("%s: bad %s view (interior %lld x %lld x %lld, pad %d, leaf stride %lld)", fn, name,
+                     (long long)nx, (long long)ny, (long long)nz, pad, (long long)leaf_stride);
+        return SG_EINVAL;
+    }
+    return SG_OK;
+}
+
+int sg_check_ptr(const char* fn, const char* name, const void* p) {
+    if (!p) {
+        sg_set_error("%s: %s is NULL", fn, name);
+        return SG_EINVAL;
+    }
+    return SG_OK;
+}
+
 int sg_check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -136,7 +159,8 @@ int sg_fill_periodic(double* field, int64_t ncomp, int64_t nx, int64_t ny, int64
     const int64_t X = nx + 2 * pad, Y = ny + 2 * pad;
     const int64_t per = ((wrap_mask & 4) ? 2 * pad * Y * X : 0) + nz * 2 * pad * X + nz * ny * 2 * pad;
     const int64_t total = per * ncomp;
-    if (total == 0 || pad == 0) return SG_OK;
+    if (total <= 0 || pad == 0) return SG_OK;
+    SG_TRY(sg_check_ptr("sg_fill_periodic", "field", field));
     sg_count_launch(1);
     fill_periodic_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         field, ncomp, nx, ny, nz, pad, wrap_mask);
@@ -152,7 +176,9 @@ int sg_gather_blocks(const double* field, int64_t nx, int64_t ny, int64_t nz, in
     }
     const int S = NIN + 2 * halo;
     const int64_t total = (int64_t)S * S * S * ncomp * nleaves;
-    if (total == 0) return SG_OK;
+    if (total <= 0) return SG_OK;
+    SG_TRY(sg_check_view("sg_gather_blocks", "field", field, nx, ny, nz, pad, leaf_stride));
+    SG_TRY(sg_check_ptr("sg_gather_blocks", "out", out));
     FieldView v = make_view(field, nx, ny, nz, pad, leaf_stride);
     sg_count_launch(1);
     gather_blocks_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(v, leaves, nleaves,
@@ -162,8 +188,14 @@ int sg_gather_blocks(const double* field, int64_t nx, int64_t ny, int64_t nz, in
 
 int sg_scale_copy(double* dst, int32_t dst_pad, const double* src, int32_t src_pad, int64_t nx, int64_t ny,
                   int64_t nz, double scale, void* stream) {
+    if (nx <= 0 || ny <= 0 || nz <= 0) return SG_OK;
+    if (dst_pad < 0 || src_pad < 0) {
+        sg_set_error("sg_scale_copy: negative pad (dst %d, src %d)", dst_pad, src_pad);
+        return SG_EINVAL;
+    }
+    SG_TRY(sg_check_ptr("sg_scale_copy", "dst", dst));
+    SG_TRY(sg_check_ptr("sg_scale_copy", "src", src));
     const int64_t total = nx * ny * nz;
-    if (total == 0) return SG_OK;
     sg_count_launch(1);
     scale_copy_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         dst, dst_pad, src, src_pad, nx, ny, nz, scale);

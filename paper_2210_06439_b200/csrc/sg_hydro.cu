@@ -676,9 +676,10 @@ int sg_reconstruct(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
         sg_set_error("sg_reconstruct: U pad must be >= 2 (got %d)", pad);
         return SG_EINVAL;
     }
-    int rc = init_tables();
-    if (rc) return rc;
     if (nleaves <= 0) return SG_OK;
+    SG_TRY(sg_check_view("sg_reconstruct", "U", U, nx, ny, nz, pad, leaf_stride));
+    SG_TRY(sg_check_ptr("sg_reconstruct", "Q", Q));
+    SG_TRY(init_tables());
     if (nleaves > 65535) {
         sg_set_error("sg_reconstruct: at most 65535 leaves per call (got %lld)", (long long)nleaves);
         return SG_EINVAL;
@@ -692,9 +693,14 @@ int sg_reconstruct(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
 
 int sg_flux(const double* Q, int64_t nleaves, double gamma, double* FX, double* FY, double* FZ,
             double* smax, uint32_t* err, uint32_t* latch, void* stream) {
-    int rc = init_tables();
-    if (rc) return rc;
     if (nleaves <= 0) return SG_OK;
+    SG_TRY(sg_check_ptr("sg_flux", "Q", Q));
+    SG_TRY(sg_check_ptr("sg_flux", "FX", FX));
+    SG_TRY(sg_check_ptr("sg_flux", "FY", FY));
+    SG_TRY(sg_check_ptr("sg_flux", "FZ", FZ));
+    SG_TRY(sg_check_ptr("sg_flux", "smax", smax));
+    SG_TRY(sg_check_ptr("sg_flux", "err", err));
+    SG_TRY(init_tables());
     sg_count_launch(1);
     flux_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax, err, latch);
     return sg_check_launch("sg_flux");
@@ -702,9 +708,14 @@ int sg_flux(const double* Q, int64_t nleaves, double gamma, double* FX, double* 
 
 int sg_flux_legacy(const double* Q, int64_t nleaves, double gamma, double* FX, double* FY, double* FZ,
                    double* smax, uint32_t* err, uint32_t* latch, void* stream) {
-    int rc = init_tables();
-    if (rc) return rc;
     if (nleaves <= 0) return SG_OK;
+    SG_TRY(sg_check_ptr("sg_flux_legacy", "Q", Q));
+    SG_TRY(sg_check_ptr("sg_flux_legacy", "FX", FX));
+    SG_TRY(sg_check_ptr("sg_flux_legacy", "FY", FY));
+    SG_TRY(sg_check_ptr("sg_flux_legacy", "FZ", FZ));
+    SG_TRY(sg_check_ptr("sg_flux_legacy", "smax", smax));
+    SG_TRY(sg_check_ptr("sg_flux_legacy", "err", err));
+    SG_TRY(init_tables());
     sg_count_launch(1);
     flux_legacy_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax,
                                                                                       err, latch);
@@ -718,9 +729,14 @@ int sg_hydro_fused(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
         sg_set_error("sg_hydro_fused: U pad must be >= 2 (got %d)", pad);
         return SG_EINVAL;
     }
-    int rc = init_tables();
-    if (rc) return rc;
     if (nleaves <= 0) return SG_OK;
+    SG_TRY(sg_check_view("sg_hydro_fused", "U", U, nx, ny, nz, pad, leaf_stride));
+    SG_TRY(sg_check_ptr("sg_hydro_fused", "FX", FX));
+    SG_TRY(sg_check_ptr("sg_hydro_fused", "FY", FY));
+    SG_TRY(sg_check_ptr("sg_hydro_fused", "FZ", FZ));
+    SG_TRY(sg_check_ptr("sg_hydro_fused", "smax", smax));
+    SG_TRY(sg_check_ptr("sg_hydro_fused", "err", err));
+    SG_TRY(init_tables());
     cudaFuncSetAttribute(hydro_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM);
     FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
     if (((uintptr_t)U & 15) || (uv.sy & 1) || (uv.sz & 1) || (uv.comp_stride & 1) || (leaf_stride & 1)) {
@@ -742,6 +758,10 @@ int sg_hydro_update(double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
                     const double* FZ, const double* smax, const double* dt_dev, double dt, double dx,
                     double cfl, uint32_t* status, uint32_t* latch, void* stream) {
     if (nleaves <= 0) return SG_OK;
+    SG_TRY(sg_check_view("sg_hydro_update", "U", U, nx, ny, nz, pad, leaf_stride));
+    SG_TRY(sg_check_ptr("sg_hydro_update", "FX", FX));
+    SG_TRY(sg_check_ptr("sg_hydro_update", "FY", FY));
+    SG_TRY(sg_check_ptr("sg_hydro_update", "FZ", FZ));
     FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
     sg_count_launch(1);
     hydro_update_kernel<<<(unsigned)nleaves, 512, 0, (cudaStream_t)stream>>>(
@@ -753,6 +773,8 @@ int sg_max_wavespeed(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_
                      const int32_t* leaves, int64_t nleaves, double gamma, double pfloor, double* smax,
                      void* stream) {
     if (nleaves <= 0) return SG_OK;
+    SG_TRY(sg_check_view("sg_max_wavespeed", "U", U, nx, ny, nz, pad, leaf_stride));
+    SG_TRY(sg_check_ptr("sg_max_wavespeed", "smax", smax));
     FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
     sg_count_launch(1);
     max_wavespeed_kernel<<<(unsigned)nleaves, 512, 0, (cudaStream_t)stream>>>(uv, leaves, gamma, pfloor, smax);
@@ -760,12 +782,16 @@ int sg_max_wavespeed(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_
 }
 
 int sg_max_reduce(const double* vals, int64_t n, double* out, void* stream) {
+    SG_TRY(sg_check_ptr("sg_max_reduce", "out", out));
+    if (n > 0) SG_TRY(sg_check_ptr("sg_max_reduce", "vals", vals));
     sg_count_launch(1);
     max_reduce_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(vals, n, out);
     return sg_check_launch("sg_max_reduce");
 }
 
 int sg_dt_from_smax(const double* s_pre, double cfl, double dx, double* dt, void* stream) {
+    SG_TRY(sg_check_ptr("sg_dt_from_smax", "s_pre", s_pre));
+    SG_TRY(sg_check_ptr("sg_dt_from_smax", "dt", dt));
     sg_count_launch(1);
     dt_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(s_pre, cfl, dx, dt);
     return sg_check_launch("sg_dt_from_smax");

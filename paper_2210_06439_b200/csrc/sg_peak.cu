@@ -32,6 +32,12 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(int iters, double a, dou
 }  // namespace sg
 
 extern "C" int sg_fp64_peak(int mode, int iters, double* sink, int64_t* flops_out, void* stream) {
+    SG_TRY(sg_check_ptr("sg_fp64_peak", "sink", sink));
+    SG_TRY(sg_check_ptr("sg_fp64_peak", "flops_out", flops_out));
+    if (iters < 0 || (mode != 0 && mode != 1)) {
+        sg_set_error("sg_fp64_peak: mode must be 0 or 1 and iters >= 0");
+        return SG_EINVAL;
+    }
     const int grid = 4 * sg_device_sm_count();
     sg_count_launch(1);
     if (mode == 0)
