@@ -1,5 +1,6 @@
 """Per-kernel device timings (CUDA events, median of reps) on the config-5
-state at level L (default 4): gravity kernels and both hydro paths."""
+state at level L (default 4): gravity kernels (precision exact|fma) and
+both hydro paths.  Usage: time_kernels.py [L] [reps] [precision]"""
 import json
 import statistics
 import sys
@@ -14,6 +15,7 @@ from paper_2210_06439_b200.kernels import GravityConfig, HydroConfig  # noqa: E4
 
 level = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+prec = sys.argv[3] if len(sys.argv) > 3 else "exact"
 u = grid.UnigridState(level, HydroConfig(), GravityConfig(theta=0.34, eps=0.5, expansion_order=1))
 u.load(scenarios.config5_state(level))
 u.set_mass()
@@ -38,8 +40,10 @@ res = {
     "fill_U": t(lambda: B.fill_periodic(u.U, 5, u.uv, 7)),
     "fill_mass": t(lambda: B.fill_periodic(u.mass, 1, u.mv, 7)),
     "cluster_aggregate": t(lambda: B.cluster_aggregate(u.mass, u.dx, u.clusters)),
-    "p2p": t(lambda: B.p2p(u.mass, u.mv, u.leaves, u.nleaves, u.dx, u.rad2, u.eps2, u.halo, u.grav, u.gv)),
-    "m2l": t(lambda: B.m2l(u.mass, u.mv, u.clusters, 0, u.leaves, u.nleaves, u.dx, u.rad2, u.eps2, 1, u.grav, u.gv)),
+    "p2p": t(lambda: B.p2p(u.mass, u.mv, u.leaves, u.nleaves, u.dx, u.rad2, u.eps2, u.halo, u.grav, u.gv,
+                           precision=prec)),
+    "m2l": t(lambda: B.m2l(u.mass, u.mv, u.clusters, 0, u.leaves, u.nleaves, u.dx, u.rad2, u.eps2, 1, u.grav, u.gv,
+                           precision=prec)),
     "reconstruct": t(lambda: B.reconstruct(u.U, u.uv, u.leaves, u.nleaves, 1e-12, u.Q)),
     "flux": t(lambda: B.flux(u.Q, u.nleaves, 1.4, u.FX, u.FY, u.FZ, u.smax, u.flux_err)),
     "hydro_fused": t(lambda: B.hydro_fused(u.U, u.uv, u.leaves, u.nleaves, 1e-12, 1.4, u.FX, u.FY, u.FZ, u.smax,
