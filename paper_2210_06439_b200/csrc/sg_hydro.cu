@@ -103,6 +103,7 @@ constexpr int REC_CELLS = NRC * NRC * NRC;
 
 __global__ void __launch_bounds__(REC_THREADS)
 reconstruct_kernel(FieldView uv, const int32_t* __restrict__ leaves, double floor_, double* __restrict__ Q) {
+    // the 4 cell blocks of a leaf are adjacent CTAs (x), sharing its U block in L2
     const int cell = blockIdx.x * REC_THREADS + threadIdx.x;
     const int64_t b = blockIdx.y;
     if (cell >= REC_CELLS) return;
@@ -680,14 +681,20 @@ int sg_reconstruct(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
     SG_TRY(sg_check_view("sg_reconstruct", "U", U, nx, ny, nz, pad, leaf_stride));
     SG_TRY(sg_check_ptr("sg_reconstruct", "Q", Q));
     SG_TRY(init_tables());
-    if (nleaves > 65535) {
-        sg_set_error("sg_reconstruct: at most 65535 leaves per call (got %lld)", (long long)nleaves);
-        return SG_EINVAL;
-    }
     FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
-    dim3 grid((REC_CELLS + REC_THREADS - 1) / REC_THREADS, (unsigned)nleaves);
-    sg_count_launch(1);
-    reconstruct_kernel<<<grid, REC_THREADS, 0, (cudaStream_t)stream>>>(uv, leaves, floor_, Q);
+    // leaves on grid.y (<= 65535 per launch): larger batches in chunks
+    constexpr int64_t CHUNK = 65535;
+    for (int64_t first = 0; first < nleaves; first += CHUNK) {
+        const int64_t n = nleaves - first < CHUNK ? nleaves - first : CHUNK;
+        FieldView v = uv;
+        const int32_t* lv = leaves;
+        if (leaves) lv += 3 * first;
+        else v.base += first * uv.leaf_stride;
+        dim3 grid((REC_CELLS + REC_THREADS - 1) / REC_THREADS, (unsigned)n);
+        sg_count_launch(1);
+        reconstruct_kernel<<<grid, REC_THREADS, 0, (cudaStream_t)stream>>>(
+            v, lv, floor_, Q + first * (int64_t)(NVAR * NDIR * REC_CELLS));
+    }
     return sg_check_launch("sg_reconstruct");
 }
 
