@@ -393,6 +393,30 @@ __device__ __forceinline__ void m2l_far(const double* __restrict__ row, int ax, 
     acc_z = add(acc_z, gz_f);
 }
 
+// the exact far term itself (compiled.py:399-418), not accumulated: rows
+// holding near clusters select between it and the near sum, then add once
+template <int ORDER>
+__device__ __forceinline__ void m2l_far_term(const double* __restrict__ row, int ax, const double4& c, double rx,
+                                             double ry, double rz, double& p_f, double& gx_f, double& gy_f,
+                                             double& gz_f) {
+    const double inv = row[ax];
+    const double inv3 = row[16 + ax];
+    p_f = -mul(c.x, inv);
+    const double gcom = mul(c.x, inv3);
+    gx_f = -mul(gcom, rx);
+    gy_f = -mul(gcom, ry);
+    gz_f = -mul(gcom, rz);
+    if (ORDER == 1) {
+        const double inv5 = row[32 + ax];
+        const double dr = add(add(mul(c.y, rx), mul(c.z, ry)), mul(c.w, rz));
+        p_f = sub(p_f, mul(dr, inv3));
+        const double t3 = mul(mul(3.0, dr), inv5);
+        gx_f = sub(add(gx_f, mul(c.y, inv3)), mul(t3, rx));
+        gy_f = sub(add(gy_f, mul(c.z, inv3)), mul(t3, ry));
+        gz_f = sub(add(gz_f, mul(c.w, inv3)), mul(t3, rz));
+    }
+}
+
 template <int ORDER, bool SMALL_NEAR, bool FAST>
 __global__ void __launch_bounds__(M2L_THREADS, 1)
 m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int64_t B, double dx,
@@ -542,8 +566,15 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
                     const int rowslot = (az * 3 + ay) * 3;
 #pragma unroll
                     for (int cx = 0; cx < NC; ++cx) {
-                        double p = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
-                        m2l_far<ORDER, FAST>(row, axv[cx], crow[cx], rxv[cx], ry, rz, p, gx, gy, gz);
+                        double p, gx, gy, gz;
+                        if (FAST) {
+                            p = gx = gy = gz = 0.0;
+                            m2l_far<ORDER, FAST>(row, axv[cx], crow[cx], rxv[cx], ry, rz, p, gx, gy, gz);
+                        } else {
+                            // the term itself: acc + t == acc + (0 + t) bitwise, since
+                            // accumulators are never -0.0
+                            m2l_far_term<ORDER>(row, axv[cx], crow[cx], rxv[cx], ry, rz, p, gx, gy, gz);
+                        }
                         if (signbit_d(row[axv[cx]])) {
                             const int k = near_slot[rowslot + axv[cx]];
                             p = wk[(k * 4 + 0) * M2L_THREADS];
@@ -886,10 +917,10 @@ m2l_terms_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leave
 #pragma unroll 1
     for (int cx = 0; cx < NC; ++cx) {
         const int ax = fold(x - 2 * cx + 7);
-        double p = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+        double p, gx, gy, gz;
         if (!signbit_d(row[ax])) {
             const double rx = mul(sub(tx, add((double)(2 * cx - 8), 1.0)), dx);
-            m2l_far<ORDER, false>(row, ax, cl[cx], rx, ry, rz, p, gx, gy, gz);
+            m2l_far_term<ORDER>(row, ax, cl[cx], rx, ry, rz, p, gx, gy, gz);
         } else if (SMALL_NEAR) {
             m2l_near_small(nm, near_tab, x, y, z, cx, cy, cz, dx, p, gx, gy, gz);
         } else {
