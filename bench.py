@@ -196,15 +196,19 @@ def m2l_traffic_from_profile():
     level 4, from the committed ncu --set full summary (profiles/)."""
     import re
     for f in sorted((REPO / "profiles").glob("r*_m2l_L4_ncu_full.txt"), reverse=True):
-        txt = f.read_text()
-        vals = {}
-        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            m = re.search(key + r"\s+([0-9.]+)\s+(\w+)", txt)
-            if m:
-                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(m.group(2), 1)
-                vals[key] = float(m.group(1)) * scale
-        if len(vals) == 2:
-            return sum(vals.values()), f.name
+        # one section per captured kernel; take the exact M2L one
+        for txt in f.read_text().split("== ncu --set full")[1:]:
+            name = re.search(r"Kernel Name\s+(.*)", txt)
+            if not name or "m2l_kernel" not in name.group(1):
+                continue
+            vals = {}
+            for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                m = re.search(key + r"\s+([0-9.]+)\s+(\w+)", txt)
+                if m:
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(m.group(2), 1)
+                    vals[key] = float(m.group(1)) * scale
+            if len(vals) == 2:
+                return sum(vals.values()), f.name
     return None, None
 
 

@@ -204,3 +204,20 @@ def test_source_cube_is_periodic_window_of_global_field():
     import pytest
     with pytest.raises(ValueError):
         octree.source_cube(nb, "mass", 9)
+
+
+def test_bench_roofline_traffic_reads_the_m2l_section():
+    """bench.py's roofline `traffic` comes from the exact-M2L section of the
+    newest committed ncu summary (the file may also hold a P2P capture)."""
+    import sys
+
+    from conftest import REPO
+    sys.path.insert(0, str(REPO))
+    import bench
+
+    traffic, name = bench.m2l_traffic_from_profile()
+    assert name is not None and name.endswith("_m2l_L4_ncu_full.txt")
+    text = (REPO / "profiles" / name).read_text()
+    sect = [t for t in text.split("== ncu --set full")[1:] if "m2l_kernel" in t.split("\n", 3)[1]]
+    assert sect, name
+    assert 1e7 < traffic < 1e9
