@@ -130,19 +130,31 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
     const int S = NIN + 2 * halo;
     const int pitch = p2p_pitch(S);
     const int plane = pitch * S;
-    double* cube = reinterpret_cast<double*>(smem_raw);
+    // two cube buffers: leaf b+G streams in (cp.async) behind leaf b's compute
+    double* const bufs = reinterpret_cast<double*>(smem_raw);
+    const int cube_sz = S * plane;
     const int tid = threadIdx.x;
     const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;  // z in 0..3; second target z + 4
     const int tcell = (z + halo) * plane + (y + halo) * pitch + (x + halo);
     const int t2 = tcell + 4 * plane;
-    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
-        __syncthreads();
-        const double* src = leaf_origin(mv, leaves, b, halo);
+    auto stage = [&](double* dst_cube, int64_t bb) {
+        const double* src = leaf_origin(mv, leaves, bb, halo);
         for (int i = tid; i < S * S * S; i += P2P_PARAM_THREADS) {
             const int cx = i % S, cy = (i / S) % S, cz = i / (S * S);
-            cube[cz * plane + cy * pitch + cx] = __ldg(src + cz * mv.sz + cy * mv.sy + cx);
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(dst_cube + cz * plane + cy * pitch + cx);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                         "l"(src + cz * mv.sz + cy * mv.sy + cx)
+                         : "memory");
         }
-        __syncthreads();
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    if (blockIdx.x < B) stage(bufs, blockIdx.x);
+    int cur = 0;
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x, cur ^= 1) {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();  // leaf b landed; everyone is done with the other buffer
+        if (b + gridDim.x < B) stage(bufs + (cur ^ 1) * cube_sz, b + gridDim.x);
+        const double* cube = bufs + cur * cube_sz;
         double ap = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
         double bp = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
 #pragma unroll 4
@@ -1076,7 +1088,7 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
                 }
             }
         }
-        const size_t smem = sizeof(double) * (size_t)S * S * p2p_pitch(S);
+        const size_t smem = 2 * sizeof(double) * (size_t)S * S * p2p_pitch(S);  // double-buffered cube
         const int64_t pgrid = nleaves < 4 * sm_count() ? nleaves : 4 * sm_count();
         auto go = [&](auto kern) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
