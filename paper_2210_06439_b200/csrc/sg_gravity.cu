@@ -119,14 +119,21 @@ __device__ int p2p_build_chunk(P2PEntry* ent, int* warp_cnt, int c0, int halo, d
     return cnt;
 }
 
-// two targets per thread, (x, y, z) and (x, y, z + 4): each uniform stencil
-// entry is loaded once for both (the kernel is issue-bound)
-constexpr int P2P_PARAM_THREADS = 256;
+// TPT targets per thread, (x, y, z0 + k*8/TPT) for k < TPT: each uniform
+// stencil entry (constant-bank loads) and its address math serve TPT pairs;
+// the FMA form (5 DP per pair) is otherwise issue-bound.  TPT = 2 or 4
+// (4: 128 threads, 96 registers; exact 0.164 ms = TPT 2, FMA 0.125 vs 0.132).
+#ifndef SG_P2P_TPT
+#define SG_P2P_TPT 4
+#endif
+constexpr int P2P_TPT = SG_P2P_TPT;
+constexpr int P2P_PARAM_THREADS = 512 / P2P_TPT;
 template <bool FAST>
 __global__ void __launch_bounds__(P2P_PARAM_THREADS, 4)
 p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, int halo, FieldView ov,
                  const __grid_constant__ P2PStencil st) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int ZS = 8 / P2P_TPT;  // z stride between a thread's targets
     const int S = NIN + 2 * halo;
     const int pitch = p2p_pitch(S);
     const int plane = pitch * S;
@@ -134,9 +141,8 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
     double* const bufs = reinterpret_cast<double*>(smem_raw);
     const int cube_sz = S * plane;
     const int tid = threadIdx.x;
-    const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;  // z in 0..3; second target z + 4
+    const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;  // z in [0, ZS); targets z + k*ZS
     const int tcell = (z + halo) * plane + (y + halo) * pitch + (x + halo);
-    const int t2 = tcell + 4 * plane;
     auto stage = [&](double* dst_cube, int64_t bb) {
         const double* src = leaf_origin(mv, leaves, bb, halo);
         for (int i = tid; i < S * S * S; i += P2P_PARAM_THREADS) {
@@ -154,45 +160,40 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();  // leaf b landed; everyone is done with the other buffer
         if (b + gridDim.x < B) stage(bufs + (cur ^ 1) * cube_sz, b + gridDim.x);
-        const double* cube = bufs + cur * cube_sz;
-        double ap = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
-        double bp = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+        const double* cube = bufs + cur * cube_sz + tcell;
+        double ap[P2P_TPT], ax[P2P_TPT], ay[P2P_TPT], az[P2P_TPT];
+#pragma unroll
+        for (int k = 0; k < P2P_TPT; ++k) ap[k] = ax[k] = ay[k] = az[k] = 0.0;
 #pragma unroll 4
         for (int e = 0; e < st.count; ++e) {
             const int d = st.delta[e];
             const double inv = st.inv[e], inv3 = st.inv3[e], rx = st.rx[e], ry = st.ry[e], rz = st.rz[e];
-            const double ma = cube[tcell + d], mb = cube[t2 + d];
-            const double ca = mul(ma, inv3), cb = mul(mb, inv3);
-            if (FAST) {  // FMA-contracted: 5 DP instructions per pair instead of 9
-                ap = __fma_rn(-ma, inv, ap);
-                ax = __fma_rn(-ca, rx, ax);
-                ay = __fma_rn(-ca, ry, ay);
-                az = __fma_rn(-ca, rz, az);
-                bp = __fma_rn(-mb, inv, bp);
-                bx = __fma_rn(-cb, rx, bx);
-                by = __fma_rn(-cb, ry, by);
-                bz = __fma_rn(-cb, rz, bz);
-            } else {
-                ap = add(ap, -mul(ma, inv));
-                ax = add(ax, -mul(ca, rx));
-                ay = add(ay, -mul(ca, ry));
-                az = add(az, -mul(ca, rz));
-                bp = add(bp, -mul(mb, inv));
-                bx = add(bx, -mul(cb, rx));
-                by = add(by, -mul(cb, ry));
-                bz = add(bz, -mul(cb, rz));
+#pragma unroll
+            for (int k = 0; k < P2P_TPT; ++k) {
+                const double m = cube[k * ZS * plane + d];
+                const double c = mul(m, inv3);
+                if (FAST) {  // FMA-contracted: 5 DP instructions per pair instead of 9
+                    ap[k] = __fma_rn(-m, inv, ap[k]);
+                    ax[k] = __fma_rn(-c, rx, ax[k]);
+                    ay[k] = __fma_rn(-c, ry, ay[k]);
+                    az[k] = __fma_rn(-c, rz, az[k]);
+                } else {
+                    ap[k] = add(ap[k], -mul(m, inv));
+                    ax[k] = add(ax[k], -mul(c, rx));
+                    ay[k] = add(ay[k], -mul(c, ry));
+                    az[k] = add(az[k], -mul(c, rz));
+                }
             }
         }
         double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy + x;
-        o[0] = ap;
-        o[ov.comp_stride] = ax;
-        o[2 * ov.comp_stride] = ay;
-        o[3 * ov.comp_stride] = az;
-        o += 4 * ov.sz;
-        o[0] = bp;
-        o[ov.comp_stride] = bx;
-        o[2 * ov.comp_stride] = by;
-        o[3 * ov.comp_stride] = bz;
+#pragma unroll
+        for (int k = 0; k < P2P_TPT; ++k) {
+            double* ok = o + k * ZS * ov.sz;
+            ok[0] = ap[k];
+            ok[ov.comp_stride] = ax[k];
+            ok[2 * ov.comp_stride] = ay[k];
+            ok[3 * ov.comp_stride] = az[k];
+        }
     }
 }
 
