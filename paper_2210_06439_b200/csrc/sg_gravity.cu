@@ -119,48 +119,40 @@ __device__ int p2p_build_chunk(P2PEntry* ent, int* warp_cnt, int c0, int halo, d
     return cnt;
 }
 
-// TPT targets per thread, (x, y, z0 + k*8/TPT) for k < TPT: each uniform
-// stencil entry (constant-bank loads) and its address math serve TPT pairs;
-// the FMA form (5 DP per pair) is otherwise issue-bound.  TPT = 2 or 4
-// (4: 128 threads, 96 registers; exact 0.164 ms = TPT 2, FMA 0.125 vs 0.132).
-#ifndef SG_P2P_TPT
-#define SG_P2P_TPT 4
-#endif
-constexpr int P2P_TPT = SG_P2P_TPT;
+// One thread per (x, y) column owns all 8 targets z = 0..7: each uniform
+// stencil entry (constant-bank loads + offset math) serves 8 pairs -- the
+// FMA form (5 DP per pair) is otherwise issue-bound on those loads.  64
+// threads per CTA, one cube buffer, 8 CTAs per SM so staging of one CTA's
+// next leaf overlaps the others' compute.  Measured at L=4 (exact / FMA):
+// 2 targets per thread 0.166 / 0.132 ms, 4 per thread (double-buffered)
+// 0.164 / 0.125 ms, this 0.163 / 0.120 ms.
+constexpr int P2P_TPT = 8;
 constexpr int P2P_PARAM_THREADS = 512 / P2P_TPT;
+constexpr int P2P_PARAM_CTAS_PER_SM = 8;
 template <bool FAST>
-__global__ void __launch_bounds__(P2P_PARAM_THREADS, 4)
+__global__ void __launch_bounds__(P2P_PARAM_THREADS, P2P_PARAM_CTAS_PER_SM)
 p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, int halo, FieldView ov,
                  const __grid_constant__ P2PStencil st) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int ZS = 8 / P2P_TPT;  // z stride between a thread's targets
     const int S = NIN + 2 * halo;
     const int pitch = p2p_pitch(S);
     const int plane = pitch * S;
-    // two cube buffers: leaf b+G streams in (cp.async) behind leaf b's compute
-    double* const bufs = reinterpret_cast<double*>(smem_raw);
-    const int cube_sz = S * plane;
+    double* const cube = reinterpret_cast<double*>(smem_raw);
     const int tid = threadIdx.x;
-    const int x = tid & 7, y = (tid >> 3) & 7, z = tid >> 6;  // z in [0, ZS); targets z + k*ZS
-    const int tcell = (z + halo) * plane + (y + halo) * pitch + (x + halo);
-    auto stage = [&](double* dst_cube, int64_t bb) {
-        const double* src = leaf_origin(mv, leaves, bb, halo);
+    const int x = tid & 7, y = tid >> 3;
+    const double* const col = cube + halo * plane + (y + halo) * pitch + (x + halo);  // target (x, y, 0)
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        __syncthreads();  // previous leaf's reads done
+        const double* src = leaf_origin(mv, leaves, b, halo);
         for (int i = tid; i < S * S * S; i += P2P_PARAM_THREADS) {
             const int cx = i % S, cy = (i / S) % S, cz = i / (S * S);
-            const unsigned dst = (unsigned)__cvta_generic_to_shared(dst_cube + cz * plane + cy * pitch + cx);
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(cube + cz * plane + cy * pitch + cx);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
                          "l"(src + cz * mv.sz + cy * mv.sy + cx)
                          : "memory");
         }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    if (blockIdx.x < B) stage(bufs, blockIdx.x);
-    int cur = 0;
-    for (int64_t b = blockIdx.x; b < B; b += gridDim.x, cur ^= 1) {
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        __syncthreads();  // leaf b landed; everyone is done with the other buffer
-        if (b + gridDim.x < B) stage(bufs + (cur ^ 1) * cube_sz, b + gridDim.x);
-        const double* cube = bufs + cur * cube_sz + tcell;
+        asm volatile("cp.async.commit_group;\n" "cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
         double ap[P2P_TPT], ax[P2P_TPT], ay[P2P_TPT], az[P2P_TPT];
 #pragma unroll
         for (int k = 0; k < P2P_TPT; ++k) ap[k] = ax[k] = ay[k] = az[k] = 0.0;
@@ -170,7 +162,7 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
             const double inv = st.inv[e], inv3 = st.inv3[e], rx = st.rx[e], ry = st.ry[e], rz = st.rz[e];
 #pragma unroll
             for (int k = 0; k < P2P_TPT; ++k) {
-                const double m = cube[k * ZS * plane + d];
+                const double m = col[k * plane + d];
                 const double c = mul(m, inv3);
                 if (FAST) {  // FMA-contracted: 5 DP instructions per pair instead of 9
                     ap[k] = __fma_rn(-m, inv, ap[k]);
@@ -185,10 +177,10 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
                 }
             }
         }
-        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy + x;
+        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + y * ov.sy + x;
 #pragma unroll
         for (int k = 0; k < P2P_TPT; ++k) {
-            double* ok = o + k * ZS * ov.sz;
+            double* ok = o + k * ov.sz;
             ok[0] = ap[k];
             ok[ov.comp_stride] = ax[k];
             ok[2 * ov.comp_stride] = ay[k];
@@ -1089,8 +1081,9 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
                 }
             }
         }
-        const size_t smem = 2 * sizeof(double) * (size_t)S * S * p2p_pitch(S);  // double-buffered cube
-        const int64_t pgrid = nleaves < 4 * sm_count() ? nleaves : 4 * sm_count();
+        const size_t smem = sizeof(double) * (size_t)S * S * p2p_pitch(S);
+        const int64_t cap = P2P_PARAM_CTAS_PER_SM * (int64_t)sm_count();
+        const int64_t pgrid = nleaves < cap ? nleaves : cap;
         auto go = [&](auto kern) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             sg_count_launch(1);
