@@ -451,7 +451,8 @@ def main():
     man_path = HERE / "manifest.json"
     man = json.loads(man_path.read_text()) if man_path.exists() else {}
     todo = args.only.split(",") if args.only else [
-        "cfg1", "tree", "hydro_random", "cfg2", "cfg4", "cfg3", "cfg5_L2", "cfg5_L4", "scenarios", "legacy"]
+        "cfg1", "tree", "hydro_random", "cfg2", "cfg4", "cfg3", "cfg5_L0", "cfg5_L1", "cfg5_L2", "cfg5_L4",
+        "scenarios", "legacy"]
     for name in todo:
         if name == "cfg5_L4" and args.skip_l4:
             continue
@@ -460,6 +461,7 @@ def main():
         {"cfg1": lambda: gravity_cfg1(), "tree": lambda: gravity_tree(),
          "hydro_random": lambda: hydro_random(), "cfg2": lambda: cfg2_p2p(man),
          "cfg3": lambda: cfg3_m2l(man), "cfg4": lambda: cfg4_hydro(man),
+         "cfg5_L0": lambda: cfg5(man, 0, "every"), "cfg5_L1": lambda: cfg5(man, 1, "every"),
          "cfg5_L2": lambda: cfg5(man, 2, "every"), "cfg5_L4": lambda: cfg5(man, 4, "last"),
          "scenarios": lambda: scenario_runs(man), "legacy": lambda: legacy(man)}[name]()
         man["_generator"] = "tests/golden/make_golden.py (reference simdgrid, numba compiled path)"

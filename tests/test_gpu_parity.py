@@ -351,6 +351,13 @@ def test_cfg5_level2_ten_steps(manifest):
     _check_cfg5(manifest["cfg5_L2"], 2)
 
 
+@pytest.mark.parametrize("level", [0, 1])
+def test_cfg5_small_levels_ten_steps(manifest, level):
+    """L=0 (one subgrid: every neighbour is itself, the 8-cell gravity pad
+    wraps the whole grid) and L=1: ten steps with gravity each step."""
+    _check_cfg5(manifest[f"cfg5_L{level}"], level)
+
+
 def test_cfg5_level4_ten_steps(manifest):
     _check_cfg5(manifest["cfg5_L4"], 4)
 
