@@ -746,8 +746,9 @@ int sg_hydro_fused(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
     SG_TRY(init_tables());
     cudaFuncSetAttribute(hydro_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FUSED_SMEM);
     FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
-    if (((uintptr_t)U & 15) || (uv.sy & 1) || (uv.sz & 1) || (uv.comp_stride & 1) || (leaf_stride & 1)) {
-        sg_set_error("sg_hydro_fused: U rows must be 16-byte aligned (even pitches, aligned base)");
+    // the leaf block's x origin is pad - 2 + 8 cx: an even pad keeps its rows 16-byte aligned
+    if (((uintptr_t)U & 15) || (pad & 1) || (uv.sy & 1) || (uv.sz & 1) || (uv.comp_stride & 1) || (leaf_stride & 1)) {
+        sg_set_error("sg_hydro_fused: U rows must be 16-byte aligned (even pad and pitches, aligned base)");
         return SG_EINVAL;
     }
     int dev = 0, nsm = 148;

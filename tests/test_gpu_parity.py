@@ -12,6 +12,7 @@ from conftest import bitwise, digest, leaf_digests, load_npz
 
 pytestmark = pytest.mark.gpu
 
+from paper_2210_06439_b200 import _lib  # noqa: E402
 from paper_2210_06439_b200 import batched as B  # noqa: E402
 from paper_2210_06439_b200 import grid as G  # noqa: E402
 from paper_2210_06439_b200 import kernels as K  # noqa: E402
@@ -581,3 +582,59 @@ def test_m2l_latency_mode_equals_persistent(theta, order):
     blk = out[:, :8, :8, :8].reshape(4, 512).cpu().numpy()
     assert bitwise(blk[:, 100:333], want[:, :8, :8, :8].reshape(4, 512)[:, 100:333])
     assert (blk[:, :100] == 7.0).all() and (blk[:, 333:] == 7.0).all()
+
+
+def test_batched_views_with_non_default_pads():
+    """The C ABI's views take any pad: mass pads 8/10/12 (even, >= 8) and U
+    pads 2/4 give the same bits as the pads grid.py uses; the fused hydro
+    kernel rejects an odd U pad (its 16-byte row copies would misalign)."""
+    level, n = 2, 32
+    dx = 1.0 / n
+    st = scenarios.config5_state(level)
+    rho = st["rho"]
+    rad2, eps2 = K.gravity_params(dx, K.GravityConfig())
+    allc = [(x, y, z) for z in range(4) for y in range(4) for x in range(4)]
+    leaves = torch.tensor(allc, dtype=torch.int32, device="cuda")
+    grav = {}
+    for pad in (8, 10, 12):
+        mv = View(n, n, n, pad)
+        m = torch.zeros(mv.padded_shape, dtype=torch.float64, device="cuda")
+        m[pad:pad + n, pad:pad + n, pad:pad + n] = dev(rho * dx ** 3)
+        B.fill_periodic(m, 1, mv, 7)
+        z_, y_, x_ = mv.padded_shape
+        cl = torch.empty((z_ // 2, y_ // 2, x_ // 2, 4), dtype=torch.float64, device="cuda")
+        B.cluster_aggregate(m, dx, cl)
+        out = torch.zeros((2, 4, n, n, n), dtype=torch.float64, device="cuda")
+        B.p2p(m, mv, leaves, 64, dx, rad2, eps2, 2, out[0], View(n, n, n, 0))
+        B.m2l(m, mv, cl, 0, leaves, 64, dx, rad2, eps2, 1, out[1], View(n, n, n, 0))
+        grav[pad] = out.cpu().numpy()
+    assert bitwise(grav[10], grav[8]) and bitwise(grav[12], grav[8])
+    hyd = {}
+    for pad in (2, 4):
+        uv = View(n, n, n, pad)
+        U = torch.zeros((5,) + uv.padded_shape, dtype=torch.float64, device="cuda")
+        U[:, pad:pad + n, pad:pad + n, pad:pad + n] = dev(np.stack([st[k] for k in octree.HYDRO_FIELDS]))
+        B.fill_periodic(U, 5, uv, 7)
+        res = []
+        for fused in (True, False):
+            FX = torch.empty((64, 5, 8, 8, 9), dtype=torch.float64, device="cuda")
+            FY = torch.empty((64, 5, 8, 9, 8), dtype=torch.float64, device="cuda")
+            FZ = torch.empty((64, 5, 9, 8, 8), dtype=torch.float64, device="cuda")
+            smax = torch.empty(64, dtype=torch.float64, device="cuda")
+            err = torch.empty(64, dtype=torch.int32, device="cuda")
+            if fused:
+                B.hydro_fused(U, uv, leaves, 64, 1e-12, 1.4, FX, FY, FZ, smax, err)
+            else:
+                Q = torch.empty((64, 5, 26, 1000), dtype=torch.float64, device="cuda")
+                B.reconstruct(U, uv, leaves, 64, 1e-12, Q)
+                B.flux(Q, 64, 1.4, FX, FY, FZ, smax, err)
+            res.append([t.cpu().numpy() for t in (FX, FY, FZ, smax)])
+        for a, b in zip(*res):
+            assert bitwise(a, b)
+        hyd[pad] = res[0]
+    for a, b in zip(hyd[2], hyd[4]):
+        assert bitwise(a, b)
+    uv3 = View(n, n, n, 3)
+    U3 = torch.zeros((5,) + uv3.padded_shape, dtype=torch.float64, device="cuda")
+    with pytest.raises(_lib.SGError, match="even pad"):
+        B.hydro_fused(U3, uv3, leaves, 64, 1e-12, 1.4, FX, FY, FZ, smax, err)
