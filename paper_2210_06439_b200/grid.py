@@ -261,31 +261,38 @@ class UnigridState:
     def check_errors(self, step: int | None = None) -> None:
         """Raise the reference's KernelError for the first failing leaf in
         Morton (leaf_iter) order, like driver._join (driver.py:83-88)."""
+        first = self._first_error(step)
+        if first is not None:
+            raise first[1]
+
+    def _first_error(self, step: int | None = None):
+        """(Morton key, KernelError) of this slab's first failing leaf, or None."""
         fl = self.flux_latch.cpu().numpy().view(np.uint32)
         up = self.upd_latch.cpu().numpy().view(np.uint32)
         bad = np.nonzero((fl != B.U32_OK) | (up != B.U32_OK))[0]
         if not len(bad):
-            return
+            return None
         coords = self.slab.global_leaf_coords().numpy()
-        b = min(bad, key=lambda i: morton_key(*coords[i], self.level))
+        key = lambda i: morton_key(*coords[i], self.level)  # noqa: E731
+        b = min(bad, key=key)
         coord = tuple(int(c) for c in coords[b])
         prefix = f"step {step}: " if step is not None else ""
         if fl[b] != B.U32_OK:
             code, cell = decode_flux_error(int(fl[b]))
             what = "density" if code == 1 else "pressure"
-            raise KernelError(f"{prefix}non-positive {what} at a quadrature point of cell "
-                              f"(x={cell % 10 + 1}, y={(cell // 10) % 10 + 1}, z={cell // 100 + 1}) "
-                              f"[extended indices] of leaf {coord}")
+            return key(b), KernelError(f"{prefix}non-positive {what} at a quadrature point of cell "
+                                       f"(x={cell % 10 + 1}, y={(cell // 10) % 10 + 1}, z={cell // 100 + 1}) "
+                                       f"[extended indices] of leaf {coord}")
         kind, detail = int(up[b]) >> 16, int(up[b]) & 0xFFFF
         if kind == 0:
-            raise KernelError(f"{prefix}dt must be positive, got {self.dt.item()}")
+            return key(b), KernelError(f"{prefix}dt must be positive, got {self.dt.item()}")
         if kind == 1:  # message of reference kernels/__init__.py:170-174
             dt, smax = self.dt.item(), float(self.smax[b].item())
-            raise KernelError(f"{prefix}CFL violation: dt={dt:g} exceeds cfl*dx/s_max="
-                              f"{self.h.cfl * self.dx / smax:g} (s_max={smax:g})")
+            return key(b), KernelError(f"{prefix}CFL violation: dt={dt:g} exceeds cfl*dx/s_max="
+                                       f"{self.h.cfl * self.dx / smax:g} (s_max={smax:g})")
         name = "rho" if kind == 2 else "E"
-        raise KernelError(f"{prefix}non-positive (or NaN) {name} after update at interior cell "
-                          f"(x={detail % 8}, y={(detail // 8) % 8}, z={detail // 64}) of leaf {coord}")
+        return key(b), KernelError(f"{prefix}non-positive (or NaN) {name} after update at interior cell "
+                                   f"(x={detail % 8}, y={(detail // 8) % 8}, z={detail // 64}) of leaf {coord}")
 
 
 class HostPipeline:
@@ -388,8 +395,11 @@ class LocalSlabs:
                 s.hydro_kernels()
 
     def check_errors(self, step: int | None = None) -> None:
-        for s in self.states:
-            s.check_errors(step)
+        """The first failing leaf in global Morton order over all slabs (the
+        reference's leaf_iter order interleaves z)."""
+        found = [e for e in (s._first_error(step) for s in self.states) if e is not None]
+        if found:
+            raise min(found, key=lambda e: e[0])[1]
 
     def fetch(self) -> dict:
         parts = [s.fetch() for s in self.states]

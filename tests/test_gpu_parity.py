@@ -638,3 +638,29 @@ def test_batched_views_with_non_default_pads():
     U3 = torch.zeros((5,) + uv3.padded_shape, dtype=torch.float64, device="cuda")
     with pytest.raises(_lib.SGError, match="even pad"):
         B.hydro_fused(U3, uv3, leaves, 64, 1e-12, 1.4, FX, FY, FZ, smax, err)
+
+
+def test_local_slabs_report_first_failing_leaf_in_morton_order():
+    """With several slabs, the reported KernelError is the reference's first
+    failing leaf in global Morton order (which interleaves z), i.e. the same
+    error a single-slab run raises -- not the first failing leaf of slab 0."""
+    st = scenarios.config5_state(2)
+    for k in st:
+        st[k] = np.array(st[k])
+    # leaf (3,3,0) (slab 0 of 4, Morton key 27) and leaf (0,0,1) (slab 1, key 4)
+    st["rho"][3, 28, 28] = np.nan
+    st["rho"][11, 3, 3] = np.nan
+    h = K.HydroConfig(gamma=1.4)
+    g = K.GravityConfig(theta=0.34, eps=0.5, expansion_order=1)
+    one = G.UnigridState(2, h, g)
+    one.load(st)
+    one.step(0, 1)
+    with pytest.raises(K.KernelError) as want:
+        one.check_errors(0)
+    four = G.LocalSlabs(2, 4, h, g)
+    four.load(st)
+    four.step(0, 1)
+    with pytest.raises(K.KernelError) as got:
+        four.check_errors(0)
+    assert str(got.value) == str(want.value)
+    assert "(0, 0, 1)" in str(want.value)
