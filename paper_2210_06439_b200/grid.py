@@ -26,7 +26,7 @@ from . import batched as B
 from .batched import View
 from .kernels import GravityConfig, HydroConfig, KernelError, decode_flux_error, gravity_halo, gravity_params
 from .octree import HYDRO_FIELDS, morton_key
-from .slab import Slab, allreduce_max_, exchange_z_halo, exchange_z_halo_local
+from .slab import Slab, allreduce_max_, exchange_z_halo, exchange_z_halo_local, first_error_across_ranks
 
 MASS_PAD = 8
 U_PAD = 2
@@ -262,6 +262,10 @@ class UnigridState:
         """Raise the reference's KernelError for the first failing leaf in
         Morton (leaf_iter) order, like driver._join (driver.py:83-88)."""
         first = self._first_error(step)
+        if self.slab.world > 1:  # every rank raises the global first error
+            c = first_error_across_ranks(None if first is None else (first[0], str(first[1])), self.slab,
+                                         self.group)
+            first = None if c is None else (c[0], KernelError(c[1]))
         if first is not None:
             raise first[1]
 

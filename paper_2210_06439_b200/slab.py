@@ -113,3 +113,16 @@ def allreduce_max_(t: torch.Tensor, slab: Slab, group=None) -> None:
     identical for every P (driver.py:170-171)."""
     if slab.world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+
+
+def first_error_across_ranks(candidate, slab: Slab, group=None):
+    """Error reporting across slabs: each rank passes its first failing
+    leaf as (Morton key, message) or None; every rank gets back the global
+    first one (the reference reports the first failing leaf in leaf_iter
+    order, driver.py:83-88, which interleaves z) or None."""
+    if slab.world == 1:
+        return candidate
+    found = [None] * slab.world
+    dist.all_gather_object(found, candidate, group=group)
+    found = [c for c in found if c is not None]
+    return min(found, key=lambda c: c[0]) if found else None

@@ -13,7 +13,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2210_06439_b200.slab import Slab, allreduce_max_, exchange_z_halo
+from paper_2210_06439_b200.slab import Slab, allreduce_max_, exchange_z_halo, first_error_across_ranks
 
 
 def _free_port() -> int:
@@ -56,3 +56,31 @@ def test_gloo_halo_exchange_matches_periodic_pad(world, level, pad):
     for rank, ok, mx in res:
         assert ok, f"rank {rank} halo mismatch"
         assert mx == world * 0.5
+
+
+def _err_worker(rank, world, port, cands, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, first_error_across_ranks(cands[rank], Slab(2, rank, world))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_first_error_across_ranks():
+    """Every rank reports the failing leaf with the smallest Morton key over
+    all slabs (rank 1's here), or None when no rank failed."""
+    ctx = mp.get_context("spawn")
+    for cands, want in (([(27, "leaf (3, 3, 0)"), (4, "leaf (0, 0, 1)"), None, (40, "x")], (4, "leaf (0, 0, 1)")),
+                        ([None, None, None, None], None)):
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_err_worker, args=(r, 4, port, cands, q)) for r in range(4)]
+        for p in procs:
+            p.start()
+        res = [q.get(timeout=120) for _ in range(4)]
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        for rank, got in res:
+            assert (tuple(got) if got is not None else None) == want, rank
