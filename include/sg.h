@@ -89,7 +89,12 @@ int sg_p2p(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
  * doubles for stacked blocks, else 0), order in {0,1}, flat interior target
  * range [i0, i1) (the reference's run(i0, i1) chunk), out view as sg_p2p.
  * workspace: device scratch of >= sg_m2l_workspace_bytes(nleaves) bytes
- * (near-field partial sums; contents are not an output). */
+ * (near-field partial sums, or for nleaves <= 4 the per-(target, cluster)
+ * terms of the latency mode, 28 MB per subgrid; contents are not an output).
+ * One workspace per concurrently running call (per stream).  Results are
+ * independent of the launch shape: batches of <= 4 subgrids run a term
+ * kernel over 144 CTAs per subgrid plus an ordered reduction, larger ones a
+ * persistent kernel; both give the same bits. */
 int64_t sg_m2l_workspace_bytes(int64_t nleaves);
 int sg_m2l(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
            const double *clusters, int64_t cluster_leaf_stride, const int32_t *leaves, int64_t nleaves,
