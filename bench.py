@@ -450,7 +450,7 @@ def run_ours(args) -> None:
     e2e_s = time.perf_counter() - t0
     u.check_errors()
     ref_out = grid.UnigridState(LEVEL, HydroConfig(gamma=1.4), GravityConfig(theta=0.34, eps=0.5, expansion_order=1),
-                                slab=slab, group=group) if args.verify_e2e else None
+                                slab=slab, group=group, precision=args.precision) if args.verify_e2e else None
     if ref_out is not None:  # the pipelined result equals load + step + fetch
         ref_out.load(state)
         ref_out.step()
