@@ -21,7 +21,9 @@
  * (reference octree.py:149-214) and run leaves in parallel on a pthread pool (the
  * analogue of the reference WorkerPool, one task per leaf).
  */
+#define _GNU_SOURCE  /* sched_getaffinity / CPU_COUNT */
 #include <math.h>
+#include <sched.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -450,6 +452,13 @@ static void *pool_worker(void *arg) {
 }
 
 int or_max_threads(void) {
+    /* the CPUs this process may run on (affinity / cgroup cpusets), not
+     * every online CPU of the host */
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof set, &set) == 0) {
+        int c = CPU_COUNT(&set);
+        if (c > 0) return c;
+    }
     long n = sysconf(_SC_NPROCESSORS_ONLN);
     return n > 0 ? (int)n : 1;
 }
