@@ -102,3 +102,72 @@ def test_hydro_random_blocks(gamma, floor, seed):
     FX2, FZ2 = torch.empty_like(FX), torch.empty_like(FZ)
     B.hydro_fused(Ud, v, None, nb, floor, gamma, FX2, FY, FZ2, smax, err)
     assert same(FX2.cpu().numpy(), FXh) and same(FZ2.cpu().numpy(), FZh)
+
+
+def test_acceptance_c1_hundred_random_subgrids_all_kernels():
+    """Reference tests/test_acceptance.py:52-97 (c1) on the CUDA path: 100
+    random subgrids through every array kernel in one stacked (drop-in
+    layout) batch each -- cluster aggregation + M2L and P2P on random 24^3
+    mass neighbourhoods (U(0,1) dx^3, 5% zeros; tests/util.py:43-50), and
+    reconstruct, flux, update and max wave speed on gentle random states with
+    a random power-of-two scale (tests/util.py:16-30) -- bitwise against the
+    oracle, subgrid by subgrid."""
+    rng = np.random.default_rng(4242)
+    nb = 100
+    dx = 1.0 / 64
+    cfg = K.GravityConfig(theta=0.34, eps=0.5, expansion_order=1)
+    rad2, eps2 = K.gravity_params(dx, cfg)
+    cubes = rng.uniform(0.0, 1.0, (nb, 24, 24, 24))
+    cubes[rng.uniform(size=cubes.shape) < 0.05] = 0.0
+    cubes *= dx ** 3
+    d = torch.from_numpy(cubes).cuda()
+    cl = torch.empty((nb, 12, 12, 12, 4), dtype=torch.float64, device="cuda")
+    B.cluster_aggregate(d, dx, cl, nb)
+    m2l = torch.zeros((nb, 4, 8, 8, 8), dtype=torch.float64, device="cuda")
+    B.m2l(d, View(8, 8, 8, 8, leaf_stride=24 ** 3), cl, 12 ** 3 * 4, None, nb, dx, rad2, eps2, 1, m2l,
+          View(8, 8, 8, 0, leaf_stride=4 * 512))
+    h = K.gravity_halo(cfg.theta)
+    sub = np.ascontiguousarray(cubes[:, 8 - h:16 + h, 8 - h:16 + h, 8 - h:16 + h])
+    S = 8 + 2 * h
+    p2p = torch.zeros((nb, 4, 8, 8, 8), dtype=torch.float64, device="cuda")
+    B.p2p(torch.from_numpy(sub).cuda(), View(8, 8, 8, h, leaf_stride=S ** 3), None, nb, dx, rad2, eps2, h, p2p,
+          View(8, 8, 8, 0, leaf_stride=4 * 512))
+    clh, m2lh, p2ph = cl.cpu().numpy(), m2l.cpu().numpy(), p2p.cpu().numpy()
+    for i in range(nb):
+        M, Dx, Dy, Dz = O.cluster_aggregate(cubes[i], dx)
+        assert same(clh[i], np.stack([M, Dx, Dy, Dz], axis=-1)), i
+        assert same(m2lh[i], O.multipole(cubes[i], dx, 0.34, 0.5, 1)), i
+        assert same(p2ph[i], O.monopole(sub[i], dx, 0.34, 0.5)), i
+    # hydro
+    scale = 2.0 ** rng.integers(-4, 5, nb)
+    U = np.empty((nb, 5, 12, 12, 12))
+    U[:, 0] = rng.uniform(0.5, 1.5, (nb, 12, 12, 12))
+    U[:, 1:4] = rng.normal(0.0, 0.1, (nb, 3, 12, 12, 12))
+    U[:, 4] = rng.uniform(2.0, 3.0, (nb, 12, 12, 12))
+    U *= scale[:, None, None, None, None]
+    gamma, floor = 1.4, 1e-12
+    dU = torch.from_numpy(U).cuda()
+    v = View(8, 8, 8, 2, leaf_stride=5 * 1728)
+    Q = torch.empty((nb, 5, 26, 1000), dtype=torch.float64, device="cuda")
+    B.reconstruct(dU, v, None, nb, floor, Q)
+    FX = torch.empty((nb, 5, 8, 8, 9), dtype=torch.float64, device="cuda")
+    FY = torch.empty((nb, 5, 8, 9, 8), dtype=torch.float64, device="cuda")
+    FZ = torch.empty((nb, 5, 9, 8, 8), dtype=torch.float64, device="cuda")
+    smax = torch.empty(nb, dtype=torch.float64, device="cuda")
+    err = torch.empty(nb, dtype=torch.int32, device="cuda")
+    B.flux(Q, nb, gamma, FX, FY, FZ, smax, err)
+    ws = torch.empty(nb, dtype=torch.float64, device="cuda")
+    B.max_wavespeed(dU, v, None, nb, gamma, floor, ws)
+    dtdx = 0.05
+    st = torch.empty(nb, dtype=torch.int32, device="cuda")
+    B.hydro_update(dU, v, None, nb, FX, FY, FZ, None, None, dtdx * dx, dx, 1e9, st)
+    Qh, FXh, FYh, FZh = Q.cpu().numpy(), FX.cpu().numpy(), FY.cpu().numpy(), FZ.cpu().numpy()
+    smh, errh, wsh, Uh = smax.cpu().numpy(), err.cpu().numpy().view(np.uint32), ws.cpu().numpy(), dU.cpu().numpy()
+    for i in range(nb):
+        q = O.reconstruct(U[i], floor)
+        assert same(Qh[i].reshape(q.shape), q), i
+        fx, fy, fz, s, code, cell = O.flux(q, gamma)
+        assert same(FXh[i], fx) and same(FYh[i], fy) and same(FZh[i], fz) and smh[i] == s, i
+        assert K.decode_flux_error(int(errh[i])) == ((0, -1) if code == 0 else (code, cell)), i
+        assert wsh[i] == O.max_wavespeed(U[i], gamma, floor), i
+        assert same(Uh[i], O.hydro_update(U[i], fx, fy, fz, dtdx)), i
