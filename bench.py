@@ -48,6 +48,12 @@ UNIT = "subgrids/s"
 M2L_FLOP = {1: 26_800_128, 0: 8_338_944}      # SURVEY.md §8(d), per subgrid
 P2P_FLOP = 423_936
 HYDRO_ITER_FLOP = 1_174_000 + 1_275_264         # reconstruct + flux
+# per-kernel roof and algorithmic work per subgrid: FP64
+# kernels against the measured DADD/DMUL issue rate, HBM kernels against the
+# measured copy bandwidth (update: U interior read + write + the three flux
+# arrays; wave speed: the U interior)
+KERNEL_ROOF = {"m2l": ("fp64", M2L_FLOP[1]), "p2p": ("fp64", P2P_FLOP), "hydro_fused": ("fp64", HYDRO_ITER_FLOP),
+               "hydro_update": ("hbm", 2 * 5 * 512 * 8 + 5 * (576 * 3) * 8), "max_wavespeed": ("hbm", 5 * 512 * 8)}
 LEVEL = 4
 
 
@@ -387,6 +393,10 @@ def run_ours(args) -> None:
     slab = Slab(LEVEL, rank, world)
     state = scenarios.config5_state(LEVEL)
     peaks = fp64_peak(torch)
+    try:
+        hbm_peak = json.loads((REPO / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] * 1e9
+    except Exception:
+        hbm_peak = 6553.0e9  # B200_PROFILING.md fallback (of fallback)
 
     u = grid.UnigridState(LEVEL, HydroConfig(gamma=1.4), GravityConfig(theta=0.34, eps=0.5, expansion_order=1),
                           slab=slab, group=group, precision=args.precision)
@@ -421,6 +431,16 @@ def run_ours(args) -> None:
         ts = [a.elapsed_time(b) * 1e-3 for a, b in evs]
         per_kernel[name] = {"launches": len(ts), "mean_ms": 1e3 * sum(ts) / len(ts),
                             "subgrids_per_s": u.nleaves * world * len(ts) / sum(ts)}
+        if name in KERNEL_ROOF:  # per GPU: this rank's subgrids over its own launch time
+            bound, work = KERNEL_ROOF[name]
+            rate = u.nleaves * len(ts) / sum(ts)
+            if bound == "fp64":
+                per_kernel[name]["roofline"] = {"bound": "fp64", "tflops": work * rate / 1e12,
+                                                "frac_fp64_issue": work * rate / (peaks["dadd_tflops"] * 1e12),
+                                                "frac_dfma_peak": work * rate / (peaks["dfma_tflops"] * 1e12)}
+            elif hbm_peak:
+                per_kernel[name]["roofline"] = {"bound": "hbm", "gbs": work * rate / 1e9,
+                                                "frac_hbm": work * rate / hbm_peak}
     u.timers = None
     t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
     if world > 1:
