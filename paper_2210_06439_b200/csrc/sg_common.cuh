@@ -12,6 +12,9 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#ifdef SG_DEBUG_BOUNDS
+#include <cstdio>
+#endif
 
 namespace sg {
 
@@ -52,6 +55,23 @@ __host__ inline FieldView make_view(const double* base, int64_t nx, int64_t ny, 
     return v;
 }
 
+// Debug builds (-DSG_DEBUG_BOUNDS, tools/debug_bounds.sh) trap on any
+// violated index precondition: the compute-sanitizer stand-in on pools
+// where the sanitizer is unavailable.  Release builds compile them out.
+#ifdef SG_DEBUG_BOUNDS
+#define SG_DASSERT(c)                                                                  \
+    do {                                                                               \
+        if (!(c)) {                                                                    \
+            printf("sg bounds check failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);   \
+            __trap();                                                                  \
+        }                                                                              \
+    } while (0)
+#else
+#define SG_DASSERT(c) \
+    do {              \
+    } while (0)
+#endif
+
 // Pointer to cell (0,0,0) of the box starting `halo` cells before leaf b's
 // interior origin.
 __device__ __forceinline__ const double* leaf_origin(const FieldView& v, const int32_t* leaves,
@@ -63,6 +83,11 @@ __device__ __forceinline__ const double* leaf_origin(const FieldView& v, const i
         cz = leaves[3 * b + 2];
     }
     int64_t ox = v.pad + NIN * cx - halo, oy = v.pad + NIN * cy - halo, oz = v.pad + NIN * cz - halo;
+    // the (8 + 2 halo)^3 box lies inside the padded view (padded dims from the pitches)
+    SG_DASSERT(ox >= 0 && oy >= 0 && oz >= 0);
+    SG_DASSERT(ox + NIN + 2 * halo <= v.sy);
+    SG_DASSERT(oy + NIN + 2 * halo <= v.sz / v.sy);
+    SG_DASSERT(oz + NIN + 2 * halo <= v.comp_stride / v.sz);
     return v.base + b * v.leaf_stride + oz * v.sz + oy * v.sy + ox;
 }
 

@@ -330,6 +330,9 @@ __device__ __forceinline__ void m2l_near_small(const double* __restrict__ nm, co
     for (int o = 0; o < 8; ++o) {
         const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
         const int si = x - (bxc + ox), sj = y - (byc + oy), sk = z - (bzc + oz);
+        SG_DASSERT(bzc + oz + 8 - NB0 >= 0 && bzc + oz + 8 - NB0 < NBW && byc + oy + 8 - NB0 >= 0 &&
+                   byc + oy + 8 - NB0 < NBW && bxc + ox + 8 - NB0 >= 0 && bxc + ox + 8 - NB0 < NBW);
+        SG_DASSERT(abs(si) < NEAR_R && abs(sj) < NEAR_R && abs(sk) < NEAR_R);
         const double m = nm[((bzc + oz + 8 - NB0) * NBW + (byc + oy + 8 - NB0)) * NBW + (bxc + ox + 8 - NB0)];
         const double2 t = near_tab[(abs(sk) * NEAR_R + abs(sj)) * NEAR_R + abs(si)];
         const bool ok = !signbit_d(t.x);
@@ -556,6 +559,7 @@ m2l_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int
             for (int cy = 0; cy < NC; ++cy) {
                 const double ry = mul(sub(ty, add((double)(2 * cy - 8), 1.0)), dx);
                 const int ay = fold(y - 2 * cy + 7);
+                SG_DASSERT(az < TAB_N && ay < TAB_N && axv[0] < TAB_N && axv[NC - 1] < TAB_N);
                 const double* row = tab + (az * TAB_N + ay) * TAB_PITCH;
                 const double4* crow = cl + (cz * NC + cy) * NC;
                 // r^2 grows with |kx|, so a row holds a near cluster iff its

@@ -429,6 +429,7 @@ __device__ __forceinline__ void fused_face(const double* __restrict__ C, int axi
         zl = j; zr = j + 1; yl = yr = i + 1; xl = xr = k + 1;
     }
     const int cl_ = (zl * NRC + yl) * NRC + xl, cr_ = (zr * NRC + yr) * NRC + xr;
+    SG_DASSERT(cl_ >= 0 && cl_ < REC_CELLS && cr_ >= 0 && cr_ < REC_CELLS);
     const uint32_t kbase = (uint32_t)((((axis * 8 + i) * 9 + j) * 9 + k) * 9);
     double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0, f4 = 0.0;
 #pragma unroll 1

@@ -1,7 +1,8 @@
 """Small cases covering every kernel for compute-sanitizer runs: level-1
 gravity + hydro (fused, unfused, legacy), the drop-in per-subgrid paths
 (single-leaf M2L split over 16 CTAs, P2P param + smem stencils), gather,
-and a 2-slab local exchange step."""
+a 2-slab local exchange step, and level-3 gravity + hydro iterations in
+both precisions (persistent M2L, FMA mirror M2L, 8-target P2P)."""
 import sys
 from pathlib import Path
 
@@ -27,5 +28,15 @@ ls = grid.LocalSlabs(1, 2)
 ls.load(scenarios.config5_state(1))
 ls.step()
 ls.check_errors()
+# persistent M2L (>= 148 subgrids), the FMA mirror kernel and the 8-target P2P
+for prec in ("exact", "fma"):
+    u = grid.UnigridState(3, K.HydroConfig(), K.GravityConfig(theta=0.34, eps=0.5, expansion_order=1), precision=prec)
+    u.load(scenarios.config5_state(3))
+    u.set_mass()
+    u.gravity_iteration()
+    u.wavespeed_dt()
+    u.hydro_iteration()
+    u.check_errors()
 torch.cuda.synchronize()
+print("sanitize cases done")
 print("sanitize cases ok")
