@@ -4,6 +4,7 @@
 # shared-memory indices, SG_DEBUG_BOUNDS), run the GPU suite and the
 # sanitize cases, restore the release library.
 set -u
+make -s -C paper_2210_06439_b200/csrc debug
 cp paper_2210_06439_b200/libsg.so /tmp/libsg_release.so
 cp paper_2210_06439_b200/libsg_debug.so paper_2210_06439_b200/libsg.so
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
