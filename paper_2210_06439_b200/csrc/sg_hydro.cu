@@ -250,6 +250,25 @@ __device__ __forceinline__ void flux_face(const double* __restrict__ Qb, int axi
     F[4 * 576] = f4;
 }
 
+// face (axis, i, j, k) of the f-th entry of the z-plane-major face order:
+// per interior plane p its 72 x-faces, 72 y-faces and the 64 z-faces below
+// it, then the 64 top z-faces
+__device__ __forceinline__ void plane_major_face(int f, int& axis, int& i, int& j, int& k) {
+    if (f < 8 * 208) {
+        const int p = f / 208, r = f % 208;
+        if (r < 72) {
+            axis = 0; i = p; j = r / 9; k = r % 9;
+        } else if (r < 144) {
+            axis = 1; i = p; j = (r - 72) / 8; k = (r - 72) % 8;
+        } else {
+            axis = 2; j = p; i = (r - 144) / 8; k = (r - 144) % 8;
+        }
+    } else {
+        const int r = f - 8 * 208;
+        axis = 2; j = 8; i = r / 8; k = r % 8;
+    }
+}
+
 __global__ void __launch_bounds__(FLUX_THREADS)
 flux_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX, double* __restrict__ FY,
             double* __restrict__ FZ, double* __restrict__ smax_out, uint32_t* __restrict__ err_out,
@@ -278,19 +297,7 @@ flux_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX,
 #pragma unroll 1
     for (int f = t; f < 3 * 576; f += FLUX_THREADS) {
         int axis, i, j, k;
-        if (f < 8 * 208) {
-            const int p = f / 208, r = f % 208;
-            if (r < 72) {
-                axis = 0; i = p; j = r / 9; k = r % 9;
-            } else if (r < 144) {
-                axis = 1; i = p; j = (r - 72) / 8; k = (r - 72) % 8;
-            } else {
-                axis = 2; j = p; i = (r - 144) / 8; k = (r - 144) % 8;
-            }
-        } else {
-            const int r = f - 8 * 208;
-            axis = 2; j = 8; i = r / 8; k = r % 8;
-        }
+        plane_major_face(f, axis, i, j, k);
         flux_face(Qb, axis, i, j, k, gamma, gm1, b, FX, FY, FZ, smax, err);
     }
     // smax >= 0 and never NaN: its bit pattern orders like an unsigned integer
@@ -314,6 +321,98 @@ flux_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX,
 // the five per-variable chains (each in (i1, i2) order) advance together.
 // err key = ((((axis*8+i)*9+j)*9+k)*9+q)*2 + check.
 // ---------------------------------------------------------------------------
+// one legacy face (reference legacy.py:63-146), states read from Q with the
+// next quadrature point's loads issued ahead (as flux_face)
+__device__ __forceinline__ void legacy_face(const double* __restrict__ Qb, int axis, int i, int j, int k,
+                                            double gamma, double gm1, int64_t b, double* __restrict__ FX,
+                                            double* __restrict__ FY, double* __restrict__ FZ, double& smax,
+                                            uint32_t& err) {
+    const int64_t VS = (int64_t)NDIR * REC_CELLS;
+    int zl, zr, yl, yr, xl, xr;
+    if (axis == 0) {
+        zl = zr = i + 1; yl = yr = j + 1; xl = k; xr = k + 1;
+    } else if (axis == 1) {
+        zl = zr = i + 1; yl = j; yr = j + 1; xl = xr = k + 1;
+    } else {
+        zl = j; zr = j + 1; yl = yr = i + 1; xl = xr = k + 1;
+    }
+    const int cl_ = (zl * NRC + yl) * NRC + xl, cr_ = (zr * NRC + yr) * NRC + xr;
+    const uint32_t kbase = (uint32_t)((((axis * 8 + i) * 9 + j) * 9 + k) * 9);
+    double acc[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    double nl[NVAR], nr[NVAR];
+    {
+        const double* pl_ = Qb + c_dplus[axis][0] * REC_CELLS + cl_;
+        const double* pr_ = Qb + c_dminus[axis][0] * REC_CELLS + cr_;
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) {
+            nl[v] = __ldg(pl_ + v * VS);
+            nr[v] = __ldg(pr_ + v * VS);
+        }
+    }
+#pragma unroll 1
+    for (int qp = 0; qp < 9; ++qp) {
+        const double w = c_simpson[qp];
+        double ql[NVAR], qr[NVAR];
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) {
+            ql[v] = nl[v];
+            qr[v] = nr[v];
+        }
+        if (qp < 8) {
+            const double* pl_ = Qb + c_dplus[axis][qp + 1] * REC_CELLS + cl_;
+            const double* pr_ = Qb + c_dminus[axis][qp + 1] * REC_CELLS + cr_;
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) {
+                nl[v] = __ldg(pl_ + v * VS);
+                nr[v] = __ldg(pr_ + v * VS);
+            }
+        }
+        const double rl = ql[0], rr = qr[0];
+        const uint32_t key = (kbase + qp) * 2;
+        if (err == 0xFFFFFFFFu && (rl <= 0.0 || rr <= 0.0)) err = ((key + 0) << 12) | (1u << 10) | (uint32_t)cl_;
+        const double kel = dvd(add(add(mul(ql[1], ql[1]), mul(ql[2], ql[2])), mul(ql[3], ql[3])), mul(2.0, rl));
+        const double ker = dvd(add(add(mul(qr[1], qr[1]), mul(qr[2], qr[2])), mul(qr[3], qr[3])), mul(2.0, rr));
+        const double pl = mul(gm1, sub(ql[4], kel));
+        const double pr = mul(gm1, sub(qr[4], ker));
+        if (err == 0xFFFFFFFFu && (pl <= 0.0 || pr <= 0.0)) err = ((key + 1) << 12) | (2u << 10) | (uint32_t)cl_;
+        const double snl = axis == 0 ? ql[1] : (axis == 1 ? ql[2] : ql[3]);
+        const double snr = axis == 0 ? qr[1] : (axis == 1 ? qr[2] : qr[3]);
+        const double vnl = dvd(snl, rl);
+        const double vnr = dvd(snr, rr);
+        const double sa = add(fabs(vnl), dsqrt(dvd(mul(gamma, pl), rl)));
+        const double sb = add(fabs(vnr), dsqrt(dvd(mul(gamma, pr), rr)));
+        const double s = sb > sa ? sb : sa;  // Python max(sa, sb)
+        if (s > smax) smax = s;
+        const double hs = mul(0.5, s);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) {
+            const double ul = ql[v], ur = qr[v];
+            double flv, frv;
+            if (v == 0) {
+                flv = mul(rl, vnl);
+                frv = mul(rr, vnr);
+            } else if (v == 4) {
+                flv = mul(add(ul, pl), vnl);
+                frv = mul(add(ur, pr), vnr);
+            } else {
+                flv = mul(ul, vnl);
+                frv = mul(ur, vnr);
+                if (v == 1 + axis) {
+                    flv = add(flv, pl);
+                    frv = add(frv, pr);
+                }
+            }
+            acc[v] = add(acc[v], mul(w, sub(mul(0.5, add(flv, frv)), mul(hs, sub(ur, ul)))));
+        }
+    }
+    double* F;
+    if (axis == 0) F = FX + b * 5 * 576 + (i * 8 + j) * 9 + k;
+    else if (axis == 1) F = FY + b * 5 * 576 + (i * 9 + j) * 8 + k;
+    else F = FZ + b * 5 * 576 + (j * 8 + i) * 8 + k;
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) F[v * 576] = acc[v];
+}
+
 __global__ void __launch_bounds__(FLUX_THREADS)
 flux_legacy_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX, double* __restrict__ FY,
                    double* __restrict__ FZ, double* __restrict__ smax_out, uint32_t* __restrict__ err_out,
@@ -328,79 +427,14 @@ flux_legacy_kernel(const double* __restrict__ Q, double gamma, double* __restric
     }
     __syncthreads();
     const double* Qb = Q + b * (int64_t)(NVAR * NDIR * REC_CELLS);
-    const int64_t VS = (int64_t)NDIR * REC_CELLS;
     const double gm1 = sub(gamma, 1.0);
     double smax = 0.0;
     uint32_t err = 0xFFFFFFFFu;
 #pragma unroll 1
-    for (int axis = 0; axis < 3; ++axis) {
-        const int nj = axis == 0 ? NIN : NIN + 1;
-        const int nk = axis == 0 ? NIN + 1 : NIN;
-        const int k = t % nk, j = (t / nk) % nj, i = t / (nk * nj);
-        int zl, zr, yl, yr, xl, xr;
-        if (axis == 0) {
-            zl = zr = i + 1; yl = yr = j + 1; xl = k; xr = k + 1;
-        } else if (axis == 1) {
-            zl = zr = i + 1; yl = j; yr = j + 1; xl = xr = k + 1;
-        } else {
-            zl = j; zr = j + 1; yl = yr = i + 1; xl = xr = k + 1;
-        }
-        const int cl_ = (zl * NRC + yl) * NRC + xl, cr_ = (zr * NRC + yr) * NRC + xr;
-        const uint32_t kbase = (uint32_t)((((axis * 8 + i) * 9 + j) * 9 + k) * 9);
-        double acc[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 1
-        for (int qp = 0; qp < 9; ++qp) {
-            const double w = c_simpson[qp];
-            const double* pl_ = Qb + c_dplus[axis][qp] * REC_CELLS + cl_;
-            const double* pr_ = Qb + c_dminus[axis][qp] * REC_CELLS + cr_;
-            double ql[NVAR], qr[NVAR];
-#pragma unroll
-            for (int v = 0; v < NVAR; ++v) {
-                ql[v] = __ldg(pl_ + v * VS);
-                qr[v] = __ldg(pr_ + v * VS);
-            }
-            const double rl = ql[0], rr = qr[0];
-            const uint32_t key = (kbase + qp) * 2;
-            if (err == 0xFFFFFFFFu && (rl <= 0.0 || rr <= 0.0)) err = ((key + 0) << 12) | (1u << 10) | (uint32_t)cl_;
-            const double kel = dvd(add(add(mul(ql[1], ql[1]), mul(ql[2], ql[2])), mul(ql[3], ql[3])), mul(2.0, rl));
-            const double ker = dvd(add(add(mul(qr[1], qr[1]), mul(qr[2], qr[2])), mul(qr[3], qr[3])), mul(2.0, rr));
-            const double pl = mul(gm1, sub(ql[4], kel));
-            const double pr = mul(gm1, sub(qr[4], ker));
-            if (err == 0xFFFFFFFFu && (pl <= 0.0 || pr <= 0.0)) err = ((key + 1) << 12) | (2u << 10) | (uint32_t)cl_;
-            const double vnl = dvd(ql[1 + axis], rl);
-            const double vnr = dvd(qr[1 + axis], rr);
-            const double sa = add(fabs(vnl), dsqrt(dvd(mul(gamma, pl), rl)));
-            const double sb = add(fabs(vnr), dsqrt(dvd(mul(gamma, pr), rr)));
-            const double s = sb > sa ? sb : sa;  // Python max(sa, sb)
-            if (s > smax) smax = s;
-            const double hs = mul(0.5, s);
-#pragma unroll
-            for (int v = 0; v < NVAR; ++v) {
-                const double ul = ql[v], ur = qr[v];
-                double flv, frv;
-                if (v == 0) {
-                    flv = mul(rl, vnl);
-                    frv = mul(rr, vnr);
-                } else if (v == 4) {
-                    flv = mul(add(ul, pl), vnl);
-                    frv = mul(add(ur, pr), vnr);
-                } else {
-                    flv = mul(ul, vnl);
-                    frv = mul(ur, vnr);
-                    if (v == 1 + axis) {
-                        flv = add(flv, pl);
-                        frv = add(frv, pr);
-                    }
-                }
-                acc[v] = add(acc[v], mul(w, sub(mul(0.5, add(flv, frv)), mul(hs, sub(ur, ul)))));
-            }
-        }
-        double* F;
-        if (axis == 0) F = FX + b * 5 * 576 + (i * 8 + j) * 9 + k;
-        else if (axis == 1) F = FY + b * 5 * 576 + (i * 9 + j) * 8 + k;
-        else F = FZ + b * 5 * 576 + (j * 8 + i) * 8 + k;
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) F[v * 576] = acc[v];
+    for (int f = t; f < 3 * 576; f += FLUX_THREADS) {
+        int axis, i, j, k;
+        plane_major_face(f, axis, i, j, k);
+        legacy_face(Qb, axis, i, j, k, gamma, gm1, b, FX, FY, FZ, smax, err);
     }
     atomicMax(&s_smax, (unsigned long long)__double_as_longlong(smax));
     if (err != 0xFFFFFFFFu) atomicMin(&s_err, err);

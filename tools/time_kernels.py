@@ -46,6 +46,7 @@ res = {
                            precision=prec)),
     "reconstruct": t(lambda: B.reconstruct(u.U, u.uv, u.leaves, u.nleaves, 1e-12, u.Q)),
     "flux": t(lambda: B.flux(u.Q, u.nleaves, 1.4, u.FX, u.FY, u.FZ, u.smax, u.flux_err)),
+    "flux_legacy": t(lambda: B.flux_legacy(u.Q, u.nleaves, 1.4, u.FX, u.FY, u.FZ, u.smax, u.flux_err)),
     "hydro_fused": t(lambda: B.hydro_fused(u.U, u.uv, u.leaves, u.nleaves, 1e-12, 1.4, u.FX, u.FY, u.FZ, u.smax,
                                            u.flux_err)),
     "max_wavespeed": t(lambda: B.max_wavespeed(u.U, u.uv, u.leaves, u.nleaves, 1.4, 1e-12, u.ws)),
