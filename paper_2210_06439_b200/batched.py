@@ -10,6 +10,7 @@ interior dims, the pad and the leaf stride (0 for one global field).
 from __future__ import annotations
 
 import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import torch
@@ -87,14 +88,17 @@ def p2p(mass, mv: View, leaves, nleaves: int, dx: float, rad2: float, eps2: floa
               ov.leaf_stride, _prec(precision), _stream())
 
 
-_WORKSPACE: dict = {}
+_WORKSPACE: "OrderedDict" = OrderedDict()
 _WORKSPACE_LOCK = threading.Lock()
+_WORKSPACE_MAX = 16  # (device, stream) entries kept; least recently used dropped
 
 
 def m2l_workspace(nleaves: int, device=None) -> torch.Tensor:
     """Cached scratch for sg_m2l, one per (device, stream): callers on
     different streams (e.g. pool threads, SURVEY.md 8(b) re-entrancy) never
-    share one; reuse on the same stream is stream-ordered.  Grows on demand."""
+    share one; reuse on the same stream is stream-ordered.  Grows on demand;
+    at most _WORKSPACE_MAX entries are kept (dropping one is safe: torch's
+    caching allocator reuses a freed block only for its own stream)."""
     need = int(_lib.load().sg_m2l_workspace_bytes(nleaves))
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     key = (dev, torch.cuda.current_stream(dev).cuda_stream)
@@ -103,6 +107,9 @@ def m2l_workspace(nleaves: int, device=None) -> torch.Tensor:
         if ws is None or ws.numel() * 8 < need:
             ws = torch.empty((need + 7) // 8, dtype=torch.float64, device=dev)
             _WORKSPACE[key] = ws
+        _WORKSPACE.move_to_end(key)
+        while len(_WORKSPACE) > _WORKSPACE_MAX:
+            _WORKSPACE.popitem(last=False)
     return ws
 
 
