@@ -435,24 +435,26 @@ def test_fused_equals_unfused_on_random_and_poisoned_blocks():
         assert bitwise(outs[1][0][i], g[f"FX{i}"]) and bitwise(outs[1][2][i], g[f"FZ{i}"])
 
 
-def test_host_pipeline_equals_load_step_fetch():
+@pytest.mark.parametrize("precision,level", [("exact", 2), ("fma", 3)])
+def test_host_pipeline_equals_load_step_fetch(precision, level):
     """grid.HostPipeline (overlapped H2D / step / D2H on pinned buffers) gives
-    exactly load + step + fetch for each independent submission."""
-    level = 2
+    exactly load + step + fetch for each independent submission, in both
+    gravity precisions (level 3: >= 148 subgrids, the FMA mirror kernel)."""
     st = scenarios.config5_state(level)
+    n = 8 << level
     inputs = []
     for scale in (1.0, 0.5, 2.0):  # power-of-two scalings: distinct but valid states
         f = {k: v * scale for k, v in st.items()}
         inputs.append(torch.from_numpy(np.stack([f[k] for k in octree.HYDRO_FIELDS])).pin_memory())
     g = K.GravityConfig(theta=0.34, eps=0.5, expansion_order=1)
-    u = G.UnigridState(level, K.HydroConfig(), g)
+    u = G.UnigridState(level, K.HydroConfig(), g, precision=precision)
     pipe = G.HostPipeline(u)
-    outs = [torch.empty((9, 32, 32, 32), dtype=torch.float64).pin_memory() for _ in inputs]
+    outs = [torch.empty((9, n, n, n), dtype=torch.float64).pin_memory() for _ in inputs]
     for hin, hout in zip(inputs, outs):
         pipe.submit(hin, hout)
     pipe.synchronize()
     for hin, hout in zip(inputs, outs):
-        ref = G.UnigridState(level, K.HydroConfig(), g)
+        ref = G.UnigridState(level, K.HydroConfig(), g, precision=precision)
         arr = hin.numpy()
         ref.load({k: arr[i] for i, k in enumerate(octree.HYDRO_FIELDS)})
         ref.step()
