@@ -31,6 +31,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -192,7 +193,18 @@ def run_reference(args) -> None:
                 "(bit-identical to it, tests/test_oracle_golden.py), all host threads; "
                 "step time extrapolated from a bounded sample",
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(_strict_json(line), allow_nan=False), flush=True)
+
+
+def _strict_json(obj):
+    """Non-finite floats -> null, so every printed line is strict JSON."""
+    if isinstance(obj, float):
+        return obj if math.isfinite(obj) else None
+    if isinstance(obj, dict):
+        return {k: _strict_json(v) for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return [_strict_json(v) for v in obj]
+    return obj
 
 
 # -- our arm ------------------------------------------------------------------------
@@ -537,7 +549,7 @@ def run_ours(args) -> None:
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                                     "sample": f"failed: {exc}"}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(_strict_json(line), allow_nan=False), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

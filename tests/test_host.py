@@ -221,3 +221,18 @@ def test_bench_roofline_traffic_reads_the_m2l_section():
     sect = [t for t in text.split("== ncu --set full")[1:] if "m2l_kernel" in t.split("\n", 3)[1]]
     assert sect, name
     assert 1e7 < traffic < 1e9
+
+
+def test_bench_line_is_strict_json():
+    """bench.py prints strict JSON: non-finite floats become null."""
+    import json
+    import math
+    import sys
+
+    from conftest import REPO
+    sys.path.insert(0, str(REPO))
+    import bench
+
+    line = {"value": float("nan"), "roofline": {"traffic": float("inf"), "frac": 0.5}, "xs": [1.0, -math.inf]}
+    out = json.dumps(bench._strict_json(line), allow_nan=False)
+    assert json.loads(out) == {"value": None, "roofline": {"traffic": None, "frac": 0.5}, "xs": [1.0, None]}
