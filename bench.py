@@ -139,6 +139,7 @@ def cpu_sample(state: dict, level: int, threads: int, m2l_leaves: int) -> dict:
     pick = np.ascontiguousarray(allc[rng.choice(len(allc), size=min(m2l_leaves, len(allc)), replace=False)])
     sample512 = np.ascontiguousarray(allc[rng.choice(len(allc), size=512, replace=False)])
     t = {}
+    w0 = time.perf_counter()
     t0 = time.perf_counter()
     O.m2l_batch(mass, dx, 0.34, 0.5, 1, pick, threads)
     t["m2l"] = len(pick) / (time.perf_counter() - t0)
@@ -151,11 +152,112 @@ def cpu_sample(state: dict, level: int, threads: int, m2l_leaves: int) -> dict:
     t0 = time.perf_counter()
     O.hydro_batch(U, 1e-12, 1.4, 1e-4, sample512, threads)
     t["hydro"] = 512 / (time.perf_counter() - t0)
+    wall = time.perf_counter() - w0
     nl = len(allc)
     step_s = 6 * (nl / t["m2l"] + nl / t["p2p"]) + nl / t["max_wavespeed"] + 3 * nl / t["hydro"]
-    return {"rates": t, "step_s": step_s, "value": nl / step_s,
+    return {"rates": t, "step_s": step_s, "value": nl / step_s, "extrapolated": True,
+            "sampled_leaves": {"m2l": len(pick), "p2p": 512, "max_wavespeed": 512, "hydro": 512},
+            "sample_wall_s": wall,
+            "omitted_phases": ["mass = rho*dx^3", "cluster_aggregate (inside the port's M2L per leaf)",
+                               "ghost exchange (9 per step)", "dt reduction"],
             "sample": f"M2L on {len(pick)} random leaves, P2P/wavespeed/hydro iteration on 512 leaves of "
-                      f"the config-5 state; full 4096-leaf step extrapolated as 6*(M2L+P2P)+ws+3*hydro"}
+                      f"the config-5 state; full 4096-leaf step extrapolated as 6*(M2L+P2P)+ws+3*hydro "
+                      f"(hydro sample at a fixed dt/dx of 1e-4)"}
+
+
+def numba_reference_sample(state: dict, level: int, threads: int, m2l_leaves: int) -> dict:
+    """The reference itself (simdgrid, numba compiled path, installed in
+    baseline/_ref by `pip install --target`) on a bounded sample of the same
+    config-5 workload, through its own WorkerPool (runtime.py:180-278, one
+    task per leaf as driver.py:164-174 spawns them) and public kernel entry
+    points (kernels/__init__.py:122-267): per-leaf M2L/P2P/hydro on sampled
+    leaves, the ghost exchanges and the wave-speed pass in full, extrapolated
+    to one 4096-leaf step.  Numba JIT compilation happens in an untimed
+    warm-up call of every kernel."""
+    ref = REPO / "baseline" / "_ref"
+    if not (ref / "simdgrid").is_dir():
+        return {"available": False, "why": "baseline/_ref/simdgrid not installed"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/sg_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        from simdgrid import kernels as RK
+        from simdgrid.octree import build_unigrid, exchange_ghosts, neighborhood27
+        from simdgrid.runtime import WorkerPool
+    except Exception as exc:  # numba missing etc.
+        return {"available": False, "why": f"import failed: {exc}"}
+    w0 = time.perf_counter()
+    tree = build_unigrid(level)
+    for leaf in tree.leaves:
+        cx, cy, cz = leaf.coord
+        sl = (slice(cz * 8, cz * 8 + 8), slice(cy * 8, cy * 8 + 8), slice(cx * 8, cx * 8 + 8))
+        for name in ("rho", "sx", "sy", "sz", "E"):
+            leaf.interior(name)[...] = state[name][sl]
+    h = RK.HydroConfig(gamma=1.4)
+    g = RK.GravityConfig(theta=0.34, eps=0.5, expansion_order=1)
+    nl = len(tree.leaves)
+    rng = np.random.default_rng(5)
+    pick = [int(i) for i in rng.choice(nl, size=min(m2l_leaves, nl), replace=False)]
+    s512 = [int(i) for i in rng.choice(nl, size=min(512, nl), replace=False)]
+    t = {}
+
+    def gravity_job(i, which):
+        src = neighborhood27(tree, i)
+        if which == "p2p":
+            RK.monopole_kernel(tree.leaves[i], src, g, "scalar")
+        else:
+            RK.multipole_kernel(tree.leaves[i], src, g, "scalar")
+
+    with WorkerPool(threads) as pool:
+        def run(fn, ids, *a):
+            futs = [pool.spawn(fn, i, *a) for i in ids]
+            for f in futs:
+                f.result()
+        tc = time.perf_counter()
+        for leaf in tree.leaves:
+            leaf.interior("mass")[...] = leaf.interior("rho") * leaf.dx ** 3
+        t["set_mass_s"] = time.perf_counter() - tc
+        tc = time.perf_counter()
+        exchange_ghosts(tree, "gravity")
+        t["exchange_gravity_s"] = time.perf_counter() - tc
+        tc = time.perf_counter()
+        exchange_ghosts(tree, "hydro")
+        t["exchange_hydro_s"] = time.perf_counter() - tc
+        # untimed JIT warm-up of every kernel on one leaf
+        gravity_job(0, "p2p")
+        gravity_job(0, "m2l")
+        s0 = RK.max_wavespeed(tree.leaves[0], h)
+        RK.flux(tree.leaves[0], RK.reconstruct(tree.leaves[0], h, "scalar"), h, "scalar")
+        tc = time.perf_counter()
+        s_pre = max(RK.max_wavespeed(leaf, h) for leaf in tree.leaves)   # driver.py:170 (serial)
+        t["max_wavespeed_s"] = time.perf_counter() - tc
+        dt = h.cfl * tree.dx / (3.0 * s_pre)
+        tc = time.perf_counter()
+        run(gravity_job, s512, "p2p")
+        t["p2p_per_leaf_s"] = (time.perf_counter() - tc) / len(s512)
+        tc = time.perf_counter()
+        run(gravity_job, pick, "m2l")
+        t["m2l_per_leaf_s"] = (time.perf_counter() - tc) / len(pick)
+
+        def hydro_job(i):
+            leaf = tree.leaves[i]
+            q = RK.reconstruct(leaf, h, "scalar")
+            fl = RK.flux(leaf, q, h, "scalar")
+            RK.hydro_update(leaf, fl, dt, h)
+        tc = time.perf_counter()
+        run(hydro_job, s512)
+        t["hydro_per_leaf_s"] = (time.perf_counter() - tc) / len(s512)
+    del s0
+    step_s = (t["set_mass_s"] + 6 * (t["exchange_gravity_s"] + nl * (t["p2p_per_leaf_s"] + t["m2l_per_leaf_s"]))
+              + t["max_wavespeed_s"] + 3 * (t["exchange_hydro_s"] + nl * t["hydro_per_leaf_s"]))
+    return {"available": True, "value": nl / step_s, "unit": UNIT, "cores": threads, "kind": "reference",
+            "step_s": step_s, "extrapolated": True, "parts": t, "sample_wall_s": time.perf_counter() - w0,
+            "sampled_leaves": {"m2l": len(pick), "p2p": len(s512), "hydro": len(s512), "max_wavespeed": nl},
+            "sample": f"reference simdgrid (numba) via WorkerPool({threads}): M2L on {len(pick)} random leaves, "
+                      f"P2P and hydro iteration (reconstruct+flux+update at the step's dt) on {len(s512)}; "
+                      f"set_mass, ghost exchanges and the serial wave-speed pass over all {nl} leaves; "
+                      f"step extrapolated as set_mass + 6*(exchange + nl*(P2P+M2L)) + ws + "
+                      f"3*(exchange + nl*hydro)"}
 
 
 def run_reference(args) -> None:
@@ -179,6 +281,7 @@ def run_reference(args) -> None:
         steps.append(r["step_s"])
     wall = time.perf_counter() - t0
     value = statistics.median(vals)
+    numba = numba_reference_sample(state, LEVEL, threads, max(8 * threads, 32))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": statistics.median(steps) * 1e3, "higher_is_better": True,
@@ -187,11 +290,16 @@ def run_reference(args) -> None:
         "config": config_dict(world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "build": kind, "sample": r["sample"], "rates": r["rates"],
-                         "wall_s_timed": wall},
+                         "extrapolated": True, "sampled_leaves": r["sampled_leaves"],
+                         "sample_wall_s": r["sample_wall_s"],
+                         "omitted_phases": r["omitted_phases"], "wall_s_timed": wall},
+        "extrapolated": True,
+        "reference_numba": numba,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference arm = the oracle's C restatement of the reference numba kernels "
-                "(bit-identical to it, tests/test_oracle_golden.py), all host threads; "
-                "step time extrapolated from a bounded sample",
+                "(bit-identical to it, tests/test_oracle_golden.py), all host threads; each step's time "
+                "is EXTRAPOLATED from a bounded sample (wall_s_timed is the real time of the timed samples); "
+                "reference_numba = the reference package itself on the same kind of sample",
     }
     print(json.dumps(_strict_json(line), allow_nan=False), flush=True)
 
@@ -398,10 +506,19 @@ def run_ours(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and local >= torch.cuda.device_count():
+        raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but only {torch.cuda.device_count()} GPU(s) visible")
     torch.cuda.set_device(local)
     group = None
     if world > 1:
+        # NCCL's own init lines (communicator, rank -> GPU, transport) on
+        # stderr, so a run's rank count is visible independently of our JSON
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dist.get_world_size() != world:
+            raise SystemExit(f"process group has {dist.get_world_size()} ranks, WORLD_SIZE={world}")
     slab = Slab(LEVEL, rank, world)
     state = scenarios.config5_state(LEVEL)
     peaks = fp64_peak(torch)
@@ -426,6 +543,11 @@ def run_ours(args) -> None:
     u.load(state)
     barrier()
     gpu_uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+    uuids = [gpu_uuid]
+    if world > 1:  # one distinct GPU per rank, or the scaling numbers mean nothing
+        uuids = [None] * world
+        dist.all_gather_object(uuids, gpu_uuid)
+    gpus_active = len(set(uuids))
     u.timers = {}
     launches0 = _lib.launch_count()
     with ClockSampler(gpu_uuid) as clk:
@@ -517,10 +639,14 @@ def run_ours(args) -> None:
     if not args.no_alt:
         alt = alt_precision_run(torch, dist, args, state, slab, group, peaks, world, barrier)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "gpus_active": gpus_active,
+        "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed * 1e3 / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "precision": args.precision,
+        "comm": ({"backend": "nccl", "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                  "ranks": world, "per_step": "6 mass + 3 U z-halo exchanges (2 sends + 2 recvs each), "
+                  "1 MAX all-reduce"} if world > 1 else None),
         "data": "synthetic config-5 IC (seedless, deterministic)",
         "config": config_dict(world),
         "e2e": {"value": total_leaves * e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -544,7 +670,12 @@ def run_ours(args) -> None:
             threads = O.max_threads()
             r = cpu_sample(state, LEVEL, threads, max(16 * threads, 64))
             line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
-                                    "build": kind, "sample": r["sample"], "rates": r["rates"]}
+                                    "build": kind, "sample": r["sample"], "rates": r["rates"],
+                                    "extrapolated": True, "sampled_leaves": r["sampled_leaves"],
+                                    "sample_wall_s": r["sample_wall_s"], "omitted_phases": r["omitted_phases"]}
+            if not args.no_numba:
+                line["cpu_baseline"]["reference_numba"] = numba_reference_sample(
+                    state, LEVEL, threads, max(8 * threads, 32))
         except Exception as exc:  # the baseline is a report, never the product
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                                     "sample": f"failed: {exc}"}
@@ -566,13 +697,44 @@ def main():
                     help="gravity arithmetic of the headline run: exact = bit-identical to the reference "
                          "(default); fma = FMA-contracted, within 1e-12 max-norm per component")
     ap.add_argument("--no-alt", action="store_true", help="skip the secondary-precision measurement")
+    ap.add_argument("--no-numba", action="store_true", help="skip the reference-package (numba) CPU sample")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    env_world = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if env_world is None and args.gpus > 1:
+        sys.exit(relaunch(args.gpus))
+    world = int(env_world or "1")
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a different "
+              f"GPU count", file=sys.stderr)
+        sys.exit(2)
+    run_ours(args)
+
+
+def relaunch(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks (one per
+    GPU) under torch.distributed.run on 127.0.0.1 and return its exit code.
+    Fails loudly when the node has fewer than N GPUs."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} requested but only {have} CUDA device(s) visible", file=sys.stderr)
+        return 3
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    print("bench.py: launching " + " ".join(cmd[2:]), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

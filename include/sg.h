@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SG_ABI_VERSION 2
+#define SG_ABI_VERSION 3
 
 /* precision modes of the gravity kernels:
  *  SG_PREC_EXACT  bit-identical to the reference (no FMA, reference order)
@@ -116,23 +116,29 @@ int sg_reconstruct(const double *U, int64_t nx, int64_t ny, int64_t nz, int32_t 
  * error in loop order packed as key<<12 | code<<10 | cell (code 1 density,
  * 2 pressure; cell = (z*10+y)*10+x in Q coordinates).  latch (nullable):
  * latch[b] = min(latch[b], err[b]) so multi-iteration device runs can be
- * checked once. */
+ * checked once.  gate (nullable) + iter: first-failing-iteration gating for
+ * multi-iteration runs (the reference raises after the first failing hydro
+ * iteration, driver.py:83-88 / 173-174): a failing leaf does
+ * prev = atomicMin(gate, iter) and latches only if prev >= iter, so once an
+ * iteration has failed, later iterations (stream-ordered launches with a
+ * larger iter) record nothing and *gate names the failing iteration. */
 int sg_flux(const double *Q, int64_t nleaves, double gamma, double *FX, double *FY, double *FZ,
-            double *smax, uint32_t *err, uint32_t *latch, void *stream);
+            double *smax, uint32_t *err, uint32_t *latch, int32_t *gate, int32_t iter, void *stream);
 
 /* Replaces the legacy straight-line flux (kernels/legacy.py:63-146; the
  * reference's legacy reconstruct is value-identical to reconstruct_kernel).
  * Outputs as sg_flux; err packs ((((axis*8+i)*9+j)*9+k)*9+q)*2 + check with
  * the LEFT cell, the legacy kernel's convention. */
 int sg_flux_legacy(const double *Q, int64_t nleaves, double gamma, double *FX, double *FY, double *FZ,
-                   double *smax, uint32_t *err, uint32_t *latch, void *stream);
+                   double *smax, uint32_t *err, uint32_t *latch, int32_t *gate, int32_t iter, void *stream);
 
 /* Fused reconstruct + flux for the batched step: same outputs, smax, err and
  * latch as sg_reconstruct followed by sg_flux (bit-identical), without
  * materialising Q.  U view as sg_reconstruct. */
 int sg_hydro_fused(const double *U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
                    const int32_t *leaves, int64_t nleaves, double floor_, double gamma, double *FX, double *FY,
-                   double *FZ, double *smax, uint32_t *err, uint32_t *latch, void *stream);
+                   double *FZ, double *smax, uint32_t *err, uint32_t *latch, int32_t *gate, int32_t iter,
+                   void *stream);
 
 /* Replaces compiled.hydro_update_kernel (compiled.py:265-278) plus the checks
  * of kernels.hydro_update (kernels/__init__.py:165-188), in place on the U
@@ -141,11 +147,15 @@ int sg_hydro_fused(const double *U, int64_t nx, int64_t ny, int64_t nz, int32_t 
  * skip the CFL check.  status[b] = 0xFFFFFFFF ok, else kind<<16 | detail:
  * kind 0 dt<=0, 1 CFL violation, 2 rho<=0/NaN at interior cell detail,
  * 3 E<=0/NaN at cell detail (first in (z,y,x) order, rho before E).
- * latch (nullable) as for sg_flux. */
+ * latch, gate, iter (nullable) as for sg_flux.  err_info (nullable,
+ * [B][2]): when leaf b latches, err_info[b] = {smax[b], dt} of that
+ * iteration, so the reference's CFL message can be rebuilt after later
+ * iterations have overwritten smax and dt. */
 int sg_hydro_update(double *U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
                     const int32_t *leaves, int64_t nleaves, const double *FX, const double *FY,
                     const double *FZ, const double *smax, const double *dt_dev, double dt, double dx,
-                    double cfl, uint32_t *status, uint32_t *latch, void *stream);
+                    double cfl, uint32_t *status, uint32_t *latch, int32_t *gate, int32_t iter,
+                    double *err_info, void *stream);
 
 /* Replaces compiled.max_wavespeed_kernel (compiled.py:454-480) called by
  * kernels.max_wavespeed (kernels/__init__.py:264-267): smax[b] per leaf. */

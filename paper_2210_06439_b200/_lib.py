@@ -10,7 +10,7 @@ import ctypes
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libsg.so"
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -29,11 +29,12 @@ SIGNATURES = {
                _p, _i64, _i64, _i64, _i64, _p, _i64, _i32, _p],
     "sg_m2l_workspace_bytes": [_i64],
     "sg_reconstruct": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _p, _p],
-    "sg_flux": [_p, _i64, _d, _p, _p, _p, _p, _p, _p, _p],
-    "sg_flux_legacy": [_p, _i64, _d, _p, _p, _p, _p, _p, _p, _p],
-    "sg_hydro_fused": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _d, _p, _p, _p, _p, _p, _p, _p],
+    "sg_flux": [_p, _i64, _d, _p, _p, _p, _p, _p, _p, _p, _i32, _p],
+    "sg_flux_legacy": [_p, _i64, _d, _p, _p, _p, _p, _p, _p, _p, _i32, _p],
+    "sg_hydro_fused": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _d, _p, _p, _p, _p, _p, _p, _p, _i32,
+                       _p],
     "sg_hydro_update": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _p, _p, _p, _p, _p, _d, _d, _d,
-                        _p, _p, _p],
+                        _p, _p, _p, _i32, _p, _p],
     "sg_max_wavespeed": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _d, _d, _p, _p],
     "sg_max_reduce": [_p, _i64, _p, _p],
     "sg_dt_from_smax": [_p, _d, _d, _p, _p],

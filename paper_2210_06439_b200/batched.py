@@ -128,30 +128,31 @@ def reconstruct(U, uv: View, leaves, nleaves: int, floor: float, Q) -> None:
               nleaves, float(floor), _f64(Q), _stream())
 
 
-def flux(Q, nleaves: int, gamma: float, FX, FY, FZ, smax, err, latch=None) -> None:
+def flux(Q, nleaves: int, gamma: float, FX, FY, FZ, smax, err, latch=None, gate=None, it: int = 0) -> None:
     _lib.call("sg_flux", _f64(Q), nleaves, float(gamma), _f64(FX), _f64(FY), _f64(FZ), _f64(smax),
-              _ptr(err), _ptr(latch), _stream())
+              _ptr(err), _ptr(latch), _ptr(gate), int(it), _stream())
 
 
-def flux_legacy(Q, nleaves: int, gamma: float, FX, FY, FZ, smax, err, latch=None) -> None:
+def flux_legacy(Q, nleaves: int, gamma: float, FX, FY, FZ, smax, err, latch=None, gate=None,
+                it: int = 0) -> None:
     """reference kernels/legacy.py flux formulation (not bitwise to flux())."""
     _lib.call("sg_flux_legacy", _f64(Q), nleaves, float(gamma), _f64(FX), _f64(FY), _f64(FZ), _f64(smax),
-              _ptr(err), _ptr(latch), _stream())
+              _ptr(err), _ptr(latch), _ptr(gate), int(it), _stream())
 
 
 def hydro_fused(U, uv: View, leaves, nleaves: int, floor: float, gamma: float, FX, FY, FZ, smax, err,
-                latch=None) -> None:
+                latch=None, gate=None, it: int = 0) -> None:
     """reconstruct + flux without materialising Q (bit-identical outputs)."""
     _lib.call("sg_hydro_fused", _f64(U), uv.nx, uv.ny, uv.nz, uv.pad, uv.leaf_stride, _ptr(leaves), nleaves,
               float(floor), float(gamma), _f64(FX), _f64(FY), _f64(FZ), _f64(smax), _ptr(err), _ptr(latch),
-              _stream())
+              _ptr(gate), int(it), _stream())
 
 
 def hydro_update(U, uv: View, leaves, nleaves: int, FX, FY, FZ, smax, dt_dev, dt: float, dx: float,
-                 cfl: float, status, latch=None) -> None:
+                 cfl: float, status, latch=None, gate=None, it: int = 0, err_info=None) -> None:
     _lib.call("sg_hydro_update", _f64(U), uv.nx, uv.ny, uv.nz, uv.pad, uv.leaf_stride, _ptr(leaves),
               nleaves, _f64(FX), _f64(FY), _f64(FZ), _ptr(smax), _ptr(dt_dev), float(dt), float(dx),
-              float(cfl), _ptr(status), _ptr(latch), _stream())
+              float(cfl), _ptr(status), _ptr(latch), _ptr(gate), int(it), _ptr(err_info), _stream())
 
 
 def max_wavespeed(U, uv: View, leaves, nleaves: int, gamma: float, pfloor: float, smax) -> None:

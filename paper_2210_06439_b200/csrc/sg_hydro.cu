@@ -88,6 +88,16 @@ static int init_tables() {
     return SG_OK;
 }
 
+// latch leaf b's error, gated on the first failing iteration (include/sg.h,
+// sg_flux): returns whether it was recorded
+__device__ __forceinline__ bool latch_error(uint32_t* latch, int64_t b, uint32_t code, int32_t* gate,
+                                            int32_t iter) {
+    if (!latch) return false;
+    if (gate && atomicMin(gate, iter) < iter) return false;
+    atomicMin(latch + b, code);
+    return true;
+}
+
 __device__ __forceinline__ double minmod(double ap, double am) {
     // compiled.py:58-62 (select semantics, NaN-preserving)
     const double mag = fabs(ap) < fabs(am) ? ap : am;
@@ -272,7 +282,7 @@ __device__ __forceinline__ void plane_major_face(int f, int& axis, int& i, int& 
 __global__ void __launch_bounds__(FLUX_THREADS)
 flux_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX, double* __restrict__ FY,
             double* __restrict__ FZ, double* __restrict__ smax_out, uint32_t* __restrict__ err_out,
-            uint32_t* __restrict__ latch) {
+            uint32_t* __restrict__ latch, int32_t* __restrict__ gate, int32_t iter) {
     __shared__ unsigned long long s_smax;
     __shared__ uint32_t s_err;
     const int64_t b = blockIdx.x;
@@ -307,7 +317,7 @@ flux_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX,
     if (t == 0) {
         smax_out[b] = __longlong_as_double((long long)s_smax);
         err_out[b] = s_err;
-        if (latch && s_err != 0xFFFFFFFFu) atomicMin(latch + b, s_err);
+        if (s_err != 0xFFFFFFFFu) latch_error(latch, b, s_err, gate, iter);
     }
 }
 
@@ -416,7 +426,7 @@ __device__ __forceinline__ void legacy_face(const double* __restrict__ Qb, int a
 __global__ void __launch_bounds__(FLUX_THREADS)
 flux_legacy_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX, double* __restrict__ FY,
                    double* __restrict__ FZ, double* __restrict__ smax_out, uint32_t* __restrict__ err_out,
-                   uint32_t* __restrict__ latch) {
+                   uint32_t* __restrict__ latch, int32_t* __restrict__ gate, int32_t iter) {
     __shared__ unsigned long long s_smax;
     __shared__ uint32_t s_err;
     const int64_t b = blockIdx.x;
@@ -442,7 +452,7 @@ flux_legacy_kernel(const double* __restrict__ Q, double gamma, double* __restric
     if (t == 0) {
         smax_out[b] = __longlong_as_double((long long)s_smax);
         err_out[b] = s_err;
-        if (latch && s_err != 0xFFFFFFFFu) atomicMin(latch + b, s_err);
+        if (s_err != 0xFFFFFFFFu) latch_error(latch, b, s_err, gate, iter);
     }
 }
 
@@ -585,7 +595,8 @@ __device__ __forceinline__ void prefetch_block(double* Us, const FieldView& uv, 
 __global__ void __launch_bounds__(FUSED_THREADS, 1)
 hydro_fused_kernel(FieldView uv, const int32_t* __restrict__ leaves, int64_t B, double floor_, double gamma,
                    double* __restrict__ FX, double* __restrict__ FY, double* __restrict__ FZ,
-                   double* __restrict__ smax_out, uint32_t* __restrict__ err_out, uint32_t* __restrict__ latch) {
+                   double* __restrict__ smax_out, uint32_t* __restrict__ err_out, uint32_t* __restrict__ latch,
+                   int32_t* __restrict__ gate, int32_t iter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* Us = reinterpret_cast<double*>(smem_raw);  // [5][12][12][12]
     double* C = Us + NVAR * 1728;                       // [20][1000]
@@ -631,7 +642,7 @@ hydro_fused_kernel(FieldView uv, const int32_t* __restrict__ leaves, int64_t B, 
         if (t == 0) {
             smax_out[b] = __longlong_as_double((long long)s_smax);
             err_out[b] = s_err;
-            if (latch && s_err != 0xFFFFFFFFu) atomicMin(latch + b, s_err);
+            if (s_err != 0xFFFFFFFFu) latch_error(latch, b, s_err, gate, iter);
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -646,7 +657,8 @@ __global__ void __launch_bounds__(512)
 hydro_update_kernel(FieldView uv, const int32_t* __restrict__ leaves, const double* __restrict__ FX,
                     const double* __restrict__ FY, const double* __restrict__ FZ,
                     const double* __restrict__ smax, const double* __restrict__ dt_dev, double dt_val,
-                    double dx, double cfl, uint32_t* __restrict__ status, uint32_t* __restrict__ latch) {
+                    double dx, double cfl, uint32_t* __restrict__ status, uint32_t* __restrict__ latch,
+                    int32_t* __restrict__ gate, int32_t iter, double* __restrict__ err_info) {
     __shared__ uint32_t s_st;
     const int64_t b = blockIdx.x;
     const int t = threadIdx.x;
@@ -680,7 +692,10 @@ hydro_update_kernel(FieldView uv, const int32_t* __restrict__ leaves, const doub
     __syncthreads();
     if (t == 0) {
         if (status) status[b] = s_st;
-        if (latch && s_st != 0xFFFFFFFFu) atomicMin(latch + b, s_st);
+        if (s_st != 0xFFFFFFFFu && latch_error(latch, b, s_st, gate, iter) && err_info) {
+            err_info[2 * b] = smax ? smax[b] : 0.0;
+            err_info[2 * b + 1] = dt;
+        }
     }
 }
 
@@ -770,7 +785,7 @@ int sg_reconstruct(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
 }
 
 int sg_flux(const double* Q, int64_t nleaves, double gamma, double* FX, double* FY, double* FZ,
-            double* smax, uint32_t* err, uint32_t* latch, void* stream) {
+            double* smax, uint32_t* err, uint32_t* latch, int32_t* gate, int32_t iter, void* stream) {
     if (nleaves <= 0) return SG_OK;
     SG_TRY(sg_check_ptr("sg_flux", "Q", Q));
     SG_TRY(sg_check_ptr("sg_flux", "FX", FX));
@@ -780,12 +795,13 @@ int sg_flux(const double* Q, int64_t nleaves, double gamma, double* FX, double* 
     SG_TRY(sg_check_ptr("sg_flux", "err", err));
     SG_TRY(init_tables());
     sg_count_launch(1);
-    flux_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax, err, latch);
+    flux_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax, err, latch,
+                                                                                gate, iter);
     return sg_check_launch("sg_flux");
 }
 
 int sg_flux_legacy(const double* Q, int64_t nleaves, double gamma, double* FX, double* FY, double* FZ,
-                   double* smax, uint32_t* err, uint32_t* latch, void* stream) {
+                   double* smax, uint32_t* err, uint32_t* latch, int32_t* gate, int32_t iter, void* stream) {
     if (nleaves <= 0) return SG_OK;
     SG_TRY(sg_check_ptr("sg_flux_legacy", "Q", Q));
     SG_TRY(sg_check_ptr("sg_flux_legacy", "FX", FX));
@@ -796,13 +812,14 @@ int sg_flux_legacy(const double* Q, int64_t nleaves, double gamma, double* FX, d
     SG_TRY(init_tables());
     sg_count_launch(1);
     flux_legacy_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax,
-                                                                                      err, latch);
+                                                                                      err, latch, gate, iter);
     return sg_check_launch("sg_flux_legacy");
 }
 
 int sg_hydro_fused(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
                    const int32_t* leaves, int64_t nleaves, double floor_, double gamma, double* FX, double* FY,
-                   double* FZ, double* smax, uint32_t* err, uint32_t* latch, void* stream) {
+                   double* FZ, double* smax, uint32_t* err, uint32_t* latch, int32_t* gate, int32_t iter,
+                   void* stream) {
     if (pad < 2) {
         sg_set_error("sg_hydro_fused: U pad must be >= 2 (got %d)", pad);
         return SG_EINVAL;
@@ -828,14 +845,15 @@ int sg_hydro_fused(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
     const int64_t grid = nleaves < nsm ? nleaves : nsm;
     sg_count_launch(1);
     hydro_fused_kernel<<<(unsigned)grid, FUSED_THREADS, FUSED_SMEM, (cudaStream_t)stream>>>(
-        uv, leaves, nleaves, floor_, gamma, FX, FY, FZ, smax, err, latch);
+        uv, leaves, nleaves, floor_, gamma, FX, FY, FZ, smax, err, latch, gate, iter);
     return sg_check_launch("sg_hydro_fused");
 }
 
 int sg_hydro_update(double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
                     const int32_t* leaves, int64_t nleaves, const double* FX, const double* FY,
                     const double* FZ, const double* smax, const double* dt_dev, double dt, double dx,
-                    double cfl, uint32_t* status, uint32_t* latch, void* stream) {
+                    double cfl, uint32_t* status, uint32_t* latch, int32_t* gate, int32_t iter,
+                    double* err_info, void* stream) {
     if (nleaves <= 0) return SG_OK;
     SG_TRY(sg_check_view("sg_hydro_update", "U", U, nx, ny, nz, pad, leaf_stride));
     SG_TRY(sg_check_ptr("sg_hydro_update", "FX", FX));
@@ -844,7 +862,7 @@ int sg_hydro_update(double* U, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     FieldView uv = make_view(U, nx, ny, nz, pad, leaf_stride);
     sg_count_launch(1);
     hydro_update_kernel<<<(unsigned)nleaves, 512, 0, (cudaStream_t)stream>>>(
-        uv, leaves, FX, FY, FZ, smax, dt_dev, dt, dx, cfl, status, latch);
+        uv, leaves, FX, FY, FZ, smax, dt_dev, dt, dx, cfl, status, latch, gate, iter, err_info);
     return sg_check_launch("sg_hydro_update");
 }
 

@@ -19,6 +19,8 @@ and dt computed on device.  Results are bit-identical to the reference loop.
 
 from __future__ import annotations
 
+import functools
+
 import numpy as np
 import torch
 
@@ -26,10 +28,24 @@ from . import batched as B
 from .batched import View
 from .kernels import GravityConfig, HydroConfig, KernelError, decode_flux_error, gravity_halo, gravity_params
 from .octree import HYDRO_FIELDS, morton_key
-from .slab import Slab, allreduce_max_, exchange_z_halo, exchange_z_halo_local, first_error_across_ranks
+from .slab import Slab, allreduce_max_, allreduce_min_int, exchange_z_halo, exchange_z_halo_local, \
+    first_error_across_ranks
 
 MASS_PAD = 8
 U_PAD = 2
+GATE_OPEN = 2 ** 31 - 1   # err_gate value while no hydro iteration has failed
+
+
+def _on_device(fn):
+    """Run a UnigridState method with its device current, so every launch
+    (batched._stream() = the current device's current stream) and every
+    scratch allocation target self.device even when the caller's current
+    device differs."""
+    @functools.wraps(fn)
+    def wrapped(self, *a, **kw):
+        with torch.cuda.device(self.device):
+            return fn(self, *a, **kw)
+    return wrapped
 
 
 class UnigridState:
@@ -52,6 +68,10 @@ class UnigridState:
             raise ValueError(f"precision must be 'exact' or 'fma', got {precision!r}")
         self.precision = precision
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if self.device.type != "cuda":
+            raise ValueError(f"UnigridState needs a CUDA device, got {self.device}")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         n, nz = self.slab.n, self.slab.nz
         self.n, self.nz = n, nz
         self.dx = 1.0 / n
@@ -87,10 +107,20 @@ class UnigridState:
         self.upd_status = torch.empty(nb, **i32)
         self.flux_latch = torch.full((nb,), -1, **i32)     # 0xFFFFFFFF
         self.upd_latch = torch.full((nb,), -1, **i32)
+        # first failing hydro iteration (include/sg.h, sg_flux `gate`): the
+        # reference raises right after it (driver.py:173-174), so errors of
+        # later iterations are not latched; err_info keeps that iteration's
+        # (smax, dt) per failing leaf for the CFL message
+        self.err_gate = torch.full((1,), GATE_OPEN, **i32)
+        self.err_info = torch.zeros((nb, 2), **f64)
+        self.hydro_iter = 0      # hydro iterations launched since load()
+        self.step_index = 0      # timesteps started since load()
+        self._iter_step = []     # hydro iteration -> timestep index
         self.timers = None  # optional {kernel: [(start, end) events]} for per-kernel timing
 
     # -- host <-> device ---------------------------------------------------
 
+    @_on_device
     def load(self, state: dict, *, global_arrays: bool = True) -> None:
         """Upload rho, sx, sy, sz, E (global (n,n,n) arrays, or this slab's
         (nz,n,n) part when global_arrays is False)."""
@@ -102,6 +132,7 @@ class UnigridState:
             self.U[v, p:p + nz, p:p + self.n, p:p + self.n].copy_(torch.from_numpy(np.ascontiguousarray(a)))
         self.reset_errors()
 
+    @_on_device
     def fetch(self) -> dict:
         p = U_PAD
         U = self.U[:, p:p + self.nz, p:p + self.n, p:p + self.n].cpu().numpy()
@@ -138,6 +169,7 @@ class UnigridState:
         for name in names:
             set_global_field(tree, name, out[name])
 
+    @_on_device
     def source_cubes(self, field: str = "mass", halo: int = 8, leaf_ids=None) -> torch.Tensor:
         """Batched octree.source_cube on the device: (B, 8+2h, 8+2h, 8+2h)
         boxes of `mass` (pad 8) or of a hydro variable (pad 2), after the
@@ -154,9 +186,14 @@ class UnigridState:
         B.gather_blocks(f, v, leaves, len(leaves), 1, halo, out)
         return out
 
+    @_on_device
     def reset_errors(self) -> None:
         self.flux_latch.fill_(-1)
         self.upd_latch.fill_(-1)
+        self.err_gate.fill_(GATE_OPEN)
+        self.hydro_iter = 0
+        self.step_index = 0
+        self._iter_step = []
 
     # -- per-kernel timing hooks -------------------------------------------
 
@@ -184,10 +221,12 @@ class UnigridState:
 
     # -- the step pieces ---------------------------------------------------
 
+    @_on_device
     def set_mass(self) -> None:
         """driver.py:165-166: mass = rho * dx**3 (Python float pow, as the reference)."""
         B.scale_copy(self.mass, MASS_PAD, self.U, U_PAD, self.n, self.n, self.nz, self.dx ** 3)
 
+    @_on_device
     def gravity_iteration(self) -> None:
         """driver.py:168-169: ghost exchange, then monopole and multipole for
         every leaf; the multipole result overwrites the monopole one in the
@@ -195,6 +234,7 @@ class UnigridState:
         self._halo(self.mass, 1, self.mv)
         self.gravity_kernels()
 
+    @_on_device
     def gravity_kernels(self) -> None:
         ev = self._t("cluster_aggregate")
         B.cluster_aggregate(self.mass, self.dx, self.clusters)
@@ -208,12 +248,14 @@ class UnigridState:
               self.g.expansion_order, self.grav, self.gv, precision=self.precision)
         self._done(ev)
 
+    @_on_device
     def wavespeed_dt(self) -> None:
         """driver.py:170-171 on device (+ MAX all-reduce across slabs)."""
         self.wavespeed_local()
         allreduce_max_(self.s_pre, self.slab, self.group)
         B.dt_from_smax(self.s_pre, self.h.cfl, self.dx, self.dt)
 
+    @_on_device
     def wavespeed_local(self) -> None:
         ev = self._t("max_wavespeed")
         B.max_wavespeed(self.U, self.uv, self.leaves, self.nleaves, self.h.gamma, self.h.positivity_floor,
@@ -221,16 +263,24 @@ class UnigridState:
         B.max_reduce(self.ws, self.nleaves, self.s_pre)
         self._done(ev)
 
+    @_on_device
     def hydro_iteration(self) -> None:
         """driver.py:173-174 / hydro_job 141-160 for every leaf."""
         self._halo(self.U, 5, self.uv)
         self.hydro_kernels()
 
+    @_on_device
     def hydro_kernels(self) -> None:
+        it = self.hydro_iter
+        if it >= GATE_OPEN:
+            raise OverflowError("hydro iteration counter exhausted; call load() or reset_errors()")
+        self.hydro_iter += 1
+        self._iter_step.append(self.step_index)
+        gate = dict(gate=self.err_gate, it=it)
         if self.fused_hydro:
             ev = self._t("hydro_fused")
             B.hydro_fused(self.U, self.uv, self.leaves, self.nleaves, self.h.positivity_floor, self.h.gamma,
-                          self.FX, self.FY, self.FZ, self.smax, self.flux_err, self.flux_latch)
+                          self.FX, self.FY, self.FZ, self.smax, self.flux_err, self.flux_latch, **gate)
             self._done(ev)
         else:
             ev = self._t("reconstruct")
@@ -239,15 +289,19 @@ class UnigridState:
             ev = self._t("flux")
             fl = B.flux_legacy if self.legacy_flux else B.flux
             fl(self.Q, self.nleaves, self.h.gamma, self.FX, self.FY, self.FZ, self.smax, self.flux_err,
-               self.flux_latch)
+               self.flux_latch, **gate)
             self._done(ev)
         ev = self._t("hydro_update")
         B.hydro_update(self.U, self.uv, self.leaves, self.nleaves, self.FX, self.FY, self.FZ, self.smax,
-                       self.dt, 0.0, self.dx, self.h.cfl, self.upd_status, self.upd_latch)
+                       self.dt, 0.0, self.dx, self.h.cfl, self.upd_status, self.upd_latch, err_info=self.err_info,
+                       **gate)
         self._done(ev)
 
+    @_on_device
     def step(self, gravity_per_step: int = 6, hydro_per_step: int = 3) -> None:
-        """One reference timestep (driver.py:163-174)."""
+        """One reference timestep (driver.py:163-174).  Errors are latched on
+        the device (first failing hydro iteration only); check_errors()
+        raises them, with that iteration's step number, at any later time."""
         if gravity_per_step:
             self.set_mass()
             for _ in range(gravity_per_step):
@@ -255,22 +309,43 @@ class UnigridState:
         self.wavespeed_dt()
         for _ in range(hydro_per_step):
             self.hydro_iteration()
+        self.step_index += 1
 
     # -- errors --------------------------------------------------------------
 
+    @_on_device
     def check_errors(self, step: int | None = None) -> None:
-        """Raise the reference's KernelError for the first failing leaf in
-        Morton (leaf_iter) order, like driver._join (driver.py:83-88)."""
-        first = self._first_error(step)
+        """Raise the reference's KernelError for the first failing hydro
+        iteration's first failing leaf in Morton (leaf_iter) order, prefixed
+        "step N: " like driver._join (driver.py:83-88).  `step` overrides the
+        recorded step number."""
+        gate = int(self.err_gate.item())
         if self.slab.world > 1:  # every rank raises the global first error
+            gate = allreduce_min_int(gate, self.slab, self.group)
+            if gate == GATE_OPEN:
+                return
+            first = self._first_error(step, gate)
             c = first_error_across_ranks(None if first is None else (first[0], str(first[1])), self.slab,
                                          self.group)
             first = None if c is None else (c[0], KernelError(c[1]))
+        else:
+            first = self._first_error(step, gate)
         if first is not None:
             raise first[1]
 
-    def _first_error(self, step: int | None = None):
-        """(Morton key, KernelError) of this slab's first failing leaf, or None."""
+    def failing_iteration(self) -> int | None:
+        """Index (since load()) of the first failing hydro iteration, or None."""
+        g = int(self.err_gate.item())
+        return None if g == GATE_OPEN else g
+
+    @_on_device
+    def _first_error(self, step: int | None = None, gate: int | None = None):
+        """(Morton key, KernelError) of this slab's first failing leaf in the
+        first failing hydro iteration `gate` (default: this slab's), or None."""
+        own = int(self.err_gate.item())
+        gate = own if gate is None else gate
+        if gate == GATE_OPEN or own != gate:  # no error here in that iteration
+            return None
         fl = self.flux_latch.cpu().numpy().view(np.uint32)
         up = self.upd_latch.cpu().numpy().view(np.uint32)
         bad = np.nonzero((fl != B.U32_OK) | (up != B.U32_OK))[0]
@@ -280,6 +355,8 @@ class UnigridState:
         key = lambda i: morton_key(*coords[i], self.level)  # noqa: E731
         b = min(bad, key=key)
         coord = tuple(int(c) for c in coords[b])
+        if step is None and gate < len(self._iter_step):
+            step = self._iter_step[gate]
         prefix = f"step {step}: " if step is not None else ""
         if fl[b] != B.U32_OK:
             code, cell = decode_flux_error(int(fl[b]))
@@ -288,10 +365,10 @@ class UnigridState:
                                        f"(x={cell % 10 + 1}, y={(cell // 10) % 10 + 1}, z={cell // 100 + 1}) "
                                        f"[extended indices] of leaf {coord}")
         kind, detail = int(up[b]) >> 16, int(up[b]) & 0xFFFF
+        smax, dt = (float(v) for v in self.err_info[b].tolist())  # that iteration's values
         if kind == 0:
-            return key(b), KernelError(f"{prefix}dt must be positive, got {self.dt.item()}")
+            return key(b), KernelError(f"{prefix}dt must be positive, got {dt}")
         if kind == 1:  # message of reference kernels/__init__.py:170-174
-            dt, smax = self.dt.item(), float(self.smax[b].item())
             return key(b), KernelError(f"{prefix}CFL violation: dt={dt:g} exceeds cfl*dx/s_max="
                                        f"{self.h.cfl * self.dx / smax:g} (s_max={smax:g})")
         name = "rho" if kind == 2 else "E"
@@ -397,11 +474,15 @@ class LocalSlabs:
             self._halo_all("U", 5, st[0].uv)
             for s in st:
                 s.hydro_kernels()
+        for s in st:
+            s.step_index += 1
 
     def check_errors(self, step: int | None = None) -> None:
-        """The first failing leaf in global Morton order over all slabs (the
-        reference's leaf_iter order interleaves z)."""
-        found = [e for e in (s._first_error(step) for s in self.states) if e is not None]
+        """The first failing hydro iteration over all slabs, and in it the
+        first failing leaf in global Morton order (the reference's leaf_iter
+        order interleaves z)."""
+        gate = min(int(s.err_gate.item()) for s in self.states)
+        found = [e for e in (s._first_error(step, gate) for s in self.states) if e is not None]
         if found:
             raise min(found, key=lambda e: e[0])[1]
 

@@ -130,3 +130,23 @@ def config5_state(level: int = 4, gamma: float = 1.4,
         "sz": np.zeros((n, n, n)),
         "E": E,
     }
+
+
+# NaN injections for the error-path parity cases (tests/golden/make_golden.py
+# "errors"): (z, y, x) global cells at level 2.  (4, 4, 30) sits one layer
+# inside the +x face of leaf (3, 0, 0), whose periodic +x neighbour is leaf
+# (0, 0, 0): minmod zeroes a NaN in the outer ghost layer, so that leaf only
+# fails once the NaN has advanced one cell -- in hydro iteration 2.  (4, 12, 12)
+# is the centre of leaf (1, 1, 0).  Morton keys: (0,0,0) 0 < (1,1,0) 3 < (3,0,0) 9.
+ERROR_CASES = {
+    "late_neighbour": ((4, 4, 30),),
+    "two_leaves": ((4, 4, 30), (4, 12, 12)),
+}
+
+
+def config5_error_state(case: str, level: int = 2) -> dict[str, np.ndarray]:
+    """config5_state(level) with rho = NaN at the ERROR_CASES[case] cells."""
+    st = {k: np.array(v) for k, v in config5_state(level).items()}
+    for z, y, x in ERROR_CASES[case]:
+        st["rho"][z, y, x] = np.nan
+    return st

@@ -69,30 +69,48 @@ class Slab:
         return c
 
 
+def _host_staged(t: torch.Tensor, group) -> bool:
+    """CUDA tensors over a non-NCCL backend (gloo: several ranks sharing one
+    GPU in the tests) travel through host copies; NCCL sends device memory."""
+    return t.is_cuda and dist.get_backend(group) != "nccl"
+
+
 def exchange_z_halo(field: torch.Tensor, pad: int, slab: Slab, group=None) -> None:
     """Fill the z pads of a padded field (ncomp, nz+2p, Y, X) from the
     periodic z-neighbour ranks.  Each rank sends its top `pad` interior
     planes up and its bottom `pad` planes down; matching is by posting order,
-    which also makes world == 2 (up == down) correct."""
+    which also makes world == 2 (up == down) correct.  One message per
+    direction: a one-component field sends its contiguous planes in place,
+    several components are packed into one buffer (a single device copy), so
+    a U exchange is 2 sends + 2 receives, not 4 per component."""
     if slab.world == 1:
         raise ValueError("single rank: use the local periodic fill")
     nz = slab.nz
     if nz < pad:
         raise ValueError(f"slab of {nz} planes is thinner than the halo ({pad})")
-    ncomp = field.shape[0]
-    ops = []
-    for c in range(ncomp):
-        f = field[c]
-        top = f[nz:nz + pad]            # interior planes [nz-pad+pad, nz+pad)
-        bottom = f[pad:2 * pad]         # interior planes [pad, 2pad)
-        lower_pad = f[0:pad]
-        upper_pad = f[nz + pad:nz + 2 * pad]
-        ops.append(dist.P2POp(dist.isend, top, slab.up, group))
-        ops.append(dist.P2POp(dist.isend, bottom, slab.down, group))
-        ops.append(dist.P2POp(dist.irecv, lower_pad, slab.down, group))
-        ops.append(dist.P2POp(dist.irecv, upper_pad, slab.up, group))
+    top = field[:, nz:nz + pad]             # interior planes [nz-pad, nz)
+    bottom = field[:, pad:2 * pad]          # interior planes [0, pad)
+    lower_pad = field[:, 0:pad]
+    upper_pad = field[:, nz + pad:nz + 2 * pad]
+    staged = _host_staged(field, group)
+    direct = field.shape[0] == 1 and not staged
+    if direct:
+        s_up, s_down, r_low, r_up = top, bottom, lower_pad, upper_pad
+    else:
+        dev = "cpu" if staged else field.device
+        s_up = top.to(dev, copy=True).contiguous()
+        s_down = bottom.to(dev, copy=True).contiguous()
+        r_low = torch.empty(s_up.shape, dtype=field.dtype, device=dev)
+        r_up = torch.empty(s_up.shape, dtype=field.dtype, device=dev)
+    ops = [dist.P2POp(dist.isend, s_up, slab.up, group),
+           dist.P2POp(dist.isend, s_down, slab.down, group),
+           dist.P2POp(dist.irecv, r_low, slab.down, group),
+           dist.P2POp(dist.irecv, r_up, slab.up, group)]
     for req in dist.batch_isend_irecv(ops):
         req.wait()
+    if not direct:
+        lower_pad.copy_(r_low)
+        upper_pad.copy_(r_up)
 
 
 def exchange_z_halo_local(fields: list, pad: int, nz: int) -> None:
@@ -111,8 +129,25 @@ def exchange_z_halo_local(fields: list, pad: int, nz: int) -> None:
 def allreduce_max_(t: torch.Tensor, slab: Slab, group=None) -> None:
     """dt reduction across ranks: MAX is order-independent, so dt is bitwise
     identical for every P (driver.py:170-171)."""
-    if slab.world > 1:
+    if slab.world == 1:
+        return
+    if _host_staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+        t.copy_(h)
+    else:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+
+
+def allreduce_min_int(v: int, slab: Slab, group=None) -> int:
+    """Global minimum of one integer per rank (the first failing hydro
+    iteration; a tensor collective, so the no-error path never pickles)."""
+    if slab.world == 1:
+        return v
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return int(t.item())
 
 
 def first_error_across_ranks(candidate, slab: Slab, group=None):

@@ -443,6 +443,33 @@ def legacy(man):
     man["legacy_scenarios"] = rec
 
 
+def error_runs(man):
+    """The reference's run_scenario (driver.py:91-189, blast: no gravity, 3
+    hydro iterations per step) on config-5 level-2 states with NaN cells
+    (scenarios.ERROR_CASES): the KernelError message it raises -- the first
+    failing hydro iteration's first failing leaf, "step N: ..." (driver.py:83-88)."""
+    import simdgrid.driver as RD
+    from simdgrid.scenarios import ScenarioConfig
+    rec = {}
+    for case in scenarios.ERROR_CASES:
+        st = scenarios.config5_error_state(case, 2)
+        tree = tree_from_global(2, st)
+        orig = RD.init_scenario
+        RD.init_scenario = lambda cfg, _t=tree: _t
+        try:
+            RD.run_scenario(ScenarioConfig("blast", max_level=2, stop_step=2), backend="scalar",
+                            threads=os.cpu_count() or 4)
+            msg = None
+        except K.KernelError as exc:
+            msg = str(exc)
+        finally:
+            RD.init_scenario = orig
+        rec[case] = {"level": 2, "steps": 2, "gamma": fhex(1.4),
+                     "input_digest": digest(np.stack([st[k] for k in FIELDS])), "message": msg}
+        print(f"    {case}: {msg}", flush=True)
+    man["errors"] = rec
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-l4", action="store_true")
@@ -452,7 +479,7 @@ def main():
     man = json.loads(man_path.read_text()) if man_path.exists() else {}
     todo = args.only.split(",") if args.only else [
         "cfg1", "tree", "hydro_random", "cfg2", "cfg4", "cfg3", "cfg5_L0", "cfg5_L1", "cfg5_L2", "cfg5_L4",
-        "scenarios", "legacy"]
+        "scenarios", "legacy", "errors"]
     for name in todo:
         if name == "cfg5_L4" and args.skip_l4:
             continue
@@ -463,7 +490,8 @@ def main():
          "cfg3": lambda: cfg3_m2l(man), "cfg4": lambda: cfg4_hydro(man),
          "cfg5_L0": lambda: cfg5(man, 0, "every"), "cfg5_L1": lambda: cfg5(man, 1, "every"),
          "cfg5_L2": lambda: cfg5(man, 2, "every"), "cfg5_L4": lambda: cfg5(man, 4, "last"),
-         "scenarios": lambda: scenario_runs(man), "legacy": lambda: legacy(man)}[name]()
+         "scenarios": lambda: scenario_runs(man), "legacy": lambda: legacy(man),
+         "errors": lambda: error_runs(man)}[name]()
         man["_generator"] = "tests/golden/make_golden.py (reference simdgrid, numba compiled path)"
         man_path.write_text(json.dumps(man, indent=1, sort_keys=True))
         print(f"[golden] {name} done in {time.time() - t0:.1f}s", flush=True)

@@ -19,7 +19,7 @@ def test_library_exports_every_header_symbol():
     lib = ctypes.CDLL(str(REPO / "paper_2210_06439_b200" / "libsg.so"))
     missing = [s for s in sorted(header_symbols()) if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.sg_abi_version() == 2
+    assert lib.sg_abi_version() == 3
 
 
 def test_binding_table_covers_header():
@@ -92,16 +92,18 @@ def test_argument_validation_without_device():
     bad("sg_reconstruct", P, 8, 8, 8, 2, 0, N, 1, 1e-12, N, N, match="Q is NULL")
     bad("sg_reconstruct", P, 8, 8, 8, 1, 0, N, 1, 1e-12, P, N, match="pad")
     for fn in ("sg_flux", "sg_flux_legacy"):
-        bad(fn, N, 1, 1.4, P, P, P, P, P, N, N, match="Q is NULL")
-        bad(fn, P, 1, 1.4, N, P, P, P, P, N, N, match="FX is NULL")
-        bad(fn, P, 1, 1.4, P, P, P, N, P, N, N, match="smax is NULL")
-        bad(fn, P, 1, 1.4, P, P, P, P, N, N, N, match="err is NULL")
-        assert getattr(L, fn)(N, 0, 1.4, N, N, N, N, N, N, N) == 0
-    bad("sg_hydro_fused", N, 8, 8, 8, 2, 0, N, 1, 1e-12, 1.4, P, P, P, P, P, N, N, match="U is NULL")
-    bad("sg_hydro_fused", P, 8, 8, 8, 2, 0, N, 1, 1e-12, 1.4, P, P, N, P, P, N, N, match="FZ is NULL")
-    bad("sg_hydro_fused", P, 8, 8, 8, 1, 0, N, 1, 1e-12, 1.4, P, P, P, P, P, N, N, match="pad")
-    bad("sg_hydro_update", P, 8, 8, 8, 2, 0, N, 1, P, N, P, N, N, 1e-3, d, 0.4, N, N, N, match="FY is NULL")
-    bad("sg_hydro_update", P, -8, 8, 8, 2, 0, N, 1, P, P, P, N, N, 1e-3, d, 0.4, N, N, N, match="bad U view")
+        bad(fn, N, 1, 1.4, P, P, P, P, P, N, N, 0, N, match="Q is NULL")
+        bad(fn, P, 1, 1.4, N, P, P, P, P, N, N, 0, N, match="FX is NULL")
+        bad(fn, P, 1, 1.4, P, P, P, N, P, N, N, 0, N, match="smax is NULL")
+        bad(fn, P, 1, 1.4, P, P, P, P, N, N, N, 0, N, match="err is NULL")
+        assert getattr(L, fn)(N, 0, 1.4, N, N, N, N, N, N, N, 0, N) == 0
+    bad("sg_hydro_fused", N, 8, 8, 8, 2, 0, N, 1, 1e-12, 1.4, P, P, P, P, P, N, N, 0, N, match="U is NULL")
+    bad("sg_hydro_fused", P, 8, 8, 8, 2, 0, N, 1, 1e-12, 1.4, P, P, N, P, P, N, N, 0, N, match="FZ is NULL")
+    bad("sg_hydro_fused", P, 8, 8, 8, 1, 0, N, 1, 1e-12, 1.4, P, P, P, P, P, N, N, 0, N, match="pad")
+    bad("sg_hydro_update", P, 8, 8, 8, 2, 0, N, 1, P, N, P, N, N, 1e-3, d, 0.4, N, N, N, 0, N, N,
+        match="FY is NULL")
+    bad("sg_hydro_update", P, -8, 8, 8, 2, 0, N, 1, P, P, P, N, N, 1e-3, d, 0.4, N, N, N, 0, N, N,
+        match="bad U view")
     bad("sg_max_wavespeed", P, 8, 8, 8, 2, 0, N, 1, 1.4, 1e-12, N, N, match="smax is NULL")
     bad("sg_max_reduce", P, 3, N, N, match="out is NULL")
     bad("sg_max_reduce", N, 3, P, N, match="vals is NULL")

@@ -65,7 +65,7 @@ class TestInitScenario:
         tree = D.init_scenario(D.ScenarioConfig(name, max_level=rec["level"], stop_step=1))
         for f, d in rec["input_digests"].items():
             if digest(global_field(tree, f)) != d:
-                pytest.skip("numpy transcendental loops differ on this host; GPU test skips too")
+                pytest.fail("input generator mismatch: numpy transcendental loops differ on this host -- the golden inputs cannot be reproduced, parity coverage would be lost")
 
 
 class TestCsv:

@@ -188,7 +188,7 @@ def test_cfg2_p2p_batched(manifest):
     m = manifest["cfg2_p2p"]
     rho = scenarios.config2_rho(1, 3)
     if digest(rho) != m["input_digest"]:
-        pytest.skip("config-2 generator differs on this host (libm); covered by test_gpu_vs_oracle")
+        pytest.fail("input generator mismatch: config-2 generator differs on this host (libm) -- the golden inputs cannot be reproduced, parity coverage would be lost")
     out = _batched_gravity(3, rho * (1.0 / 64) ** 3, "p2p", 0.34, 0)
     assert leaf_digests(3, out) == m["leaf_digests"]
     assert digest(out) == m["output_digest"]
@@ -199,7 +199,7 @@ def test_cfg3_m2l_batched(manifest, order):
     m = manifest["cfg3_m2l"]
     rho = scenarios.config3_rho(3)
     if digest(rho) != m["input_digest"]:
-        pytest.skip("config-3 generator differs on this host (libm)")
+        pytest.fail("input generator mismatch: config-3 generator differs on this host (libm) -- the golden inputs cannot be reproduced, parity coverage would be lost")
     out = _batched_gravity(3, rho * (1.0 / 64) ** 3, "m2l", 0.34, order)
     got = leaf_digests(3, out)
     want = m[f"o{order}"]["leaf_digests"]
@@ -329,7 +329,7 @@ def _check_cfg5(m, level, gravity_per_step=6):
     st = scenarios.config5_state(level)
     U = np.stack([st[k] for k in octree.HYDRO_FIELDS])
     if digest(U) != m["input_digest"]:
-        pytest.skip("config-5 generator differs on this host (libm)")
+        pytest.fail("input generator mismatch: config-5 generator differs on this host (libm) -- the golden inputs cannot be reproduced, parity coverage would be lost")
     u = G.UnigridState(level, K.HydroConfig(gamma=float.fromhex(m["gamma"])),
                        K.GravityConfig(theta=0.34, eps=0.5, expansion_order=1))
     u.load(st)
@@ -371,7 +371,7 @@ def test_cfg5_slabs_match_golden(manifest, level, world):
     st = scenarios.config5_state(level)
     U = np.stack([st[k] for k in octree.HYDRO_FIELDS])
     if digest(U) != m["input_digest"]:
-        pytest.skip("config-5 generator differs on this host (libm)")
+        pytest.fail("input generator mismatch: config-5 generator differs on this host (libm) -- the golden inputs cannot be reproduced, parity coverage would be lost")
     ls = G.LocalSlabs(level, world, K.HydroConfig(gamma=float.fromhex(m["gamma"])),
                       K.GravityConfig(theta=0.34, eps=0.5, expansion_order=1))
     ls.load(st)
@@ -472,7 +472,7 @@ def test_batched_kernels_on_permuted_leaf_subsets(manifest):
     rho = scenarios.config3_rho(level)
     m = manifest["cfg3_m2l"]
     if digest(rho) != m["input_digest"]:
-        pytest.skip("config-3 generator differs on this host")
+        pytest.fail("input generator mismatch: config-3 generator differs on this host -- the golden inputs cannot be reproduced, parity coverage would be lost")
     mv = View(n, n, n, 8)
     mass = torch.zeros(mv.padded_shape, dtype=torch.float64, device="cuda")
     mass[8:8 + n, 8:8 + n, 8:8 + n] = dev(rho * (1.0 / 64) ** 3)
@@ -537,7 +537,7 @@ def test_run_steps_public_entry(manifest):
     m = manifest["cfg5_L2"]
     st = scenarios.config5_state(2)
     if digest(np.stack([st[k] for k in octree.HYDRO_FIELDS])) != m["input_digest"]:
-        pytest.skip("config-5 generator differs on this host")
+        pytest.fail("input generator mismatch: config-5 generator differs on this host -- the golden inputs cannot be reproduced, parity coverage would be lost")
     out, dts = G.run_steps(st, 2, 10, hydro=K.HydroConfig(gamma=1.4),
                            gravity=K.GravityConfig(theta=0.34, eps=0.5, expansion_order=1))
     assert [d.hex() for d in dts] == m["dts"]
