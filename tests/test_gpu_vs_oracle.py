@@ -98,10 +98,72 @@ def test_hydro_random_blocks(gamma, floor, seed):
         assert same(FXh[i], fx) and same(FYh[i], fy) and same(FZh[i], fz), i
         assert K.decode_flux_error(int(err[i].cpu().numpy().view(np.uint32))) == (code, cell), i
         assert same(smax[i].item(), s) and same(ws[i].item(), O.max_wavespeed(U, gamma, floor)), i
-    # fused path on the same blocks
-    FX2, FZ2 = torch.empty_like(FX), torch.empty_like(FZ)
-    B.hydro_fused(Ud, v, None, nb, floor, gamma, FX2, FY, FZ2, smax, err)
-    assert same(FX2.cpu().numpy(), FXh) and same(FZ2.cpu().numpy(), FZh)
+    # fused path on the same blocks: fluxes, smax and first error
+    FX2, FY2, FZ2 = torch.empty_like(FX), torch.empty_like(FY), torch.empty_like(FZ)
+    smax2, err2 = torch.empty_like(smax), torch.empty_like(err)
+    B.hydro_fused(Ud, v, None, nb, floor, gamma, FX2, FY2, FZ2, smax2, err2)
+    assert same(FX2.cpu().numpy(), FXh) and same(FY2.cpu().numpy(), FYh) and same(FZ2.cpu().numpy(), FZh)
+    assert same(smax2.cpu().numpy(), smax.cpu().numpy())
+    assert np.array_equal(err2.cpu().numpy(), err.cpu().numpy())
+
+
+def _error_blocks(nb, seed, gamma):
+    """nb random hydro blocks; every 7th one poisoned so the flux raises:
+    negative pressure (code 2), non-positive density (code 1, needs
+    floor <= 0), NaN, several errors in one block (first-error order)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(nb):
+        rho = 1.0 + 0.5 * rng.uniform(-1, 1, (12, 12, 12))
+        v = rng.uniform(-1, 1, (3, 12, 12, 12))
+        p = 1.0 + 0.5 * rng.uniform(-1, 1, (12, 12, 12))
+        U = np.stack([rho, rho * v[0], rho * v[1], rho * v[2], p / (gamma - 1.0) + 0.5 * rho * (v ** 2).sum(0)])
+        kind = i % 7
+        z, y, x = rng.integers(1, 11, 3)
+        if kind == 1:                       # kinetic energy above total energy: p < 0
+            U[1, z, y, x] = 50.0
+        elif kind == 2:                     # negative density (floor 0 keeps it)
+            U[0, z, y, x] = -0.5
+        elif kind == 3:
+            U[0, z, y, x] = np.nan
+        elif kind == 4:                     # two faults, the lower key wins
+            U[1, z, y, x] = 50.0
+            U[0, 11 - z, 11 - y, 11 - x] = -0.5
+        elif kind == 5 and i % 2:           # fault on the ring only (ghost cell)
+            U[2, 0, y, x] = 80.0
+        out.append(U)
+    return np.stack(out)
+
+
+@pytest.mark.parametrize("nb,floor", [(40, 0.0), (333, 0.0), (333, 1e-12)])
+def test_fused_hydro_errors_match_unfused(nb, floor):
+    """The deduplicated fused kernel against reconstruct + flux (checked
+    bitwise against the oracle above) on batches with poisoned blocks:
+    fluxes, smax and the first-error word for every leaf, including batches
+    larger than the persistent grid (several leaves per CTA, error flush at
+    leaf boundaries)."""
+    gamma = 1.4
+    U = _error_blocks(nb, 11 + nb, gamma)
+    Ud = torch.from_numpy(U).cuda()
+    v = View(8, 8, 8, 2, leaf_stride=5 * 1728)
+    Q = torch.empty((nb, 5, 26, 1000), dtype=torch.float64, device="cuda")
+    shp = dict(dtype=torch.float64, device="cuda")
+    F1 = [torch.empty((nb, 5, 8, 8, 9), **shp), torch.empty((nb, 5, 8, 9, 8), **shp),
+          torch.empty((nb, 5, 9, 8, 8), **shp)]
+    F2 = [torch.empty_like(f) for f in F1]
+    s1, s2 = torch.empty(nb, **shp), torch.empty(nb, **shp)
+    e1 = torch.empty(nb, dtype=torch.int32, device="cuda")
+    e2 = torch.empty_like(e1)
+    B.reconstruct(Ud, v, None, nb, floor, Q)
+    B.flux(Q, nb, gamma, *F1, s1, e1)
+    B.hydro_fused(Ud, v, None, nb, floor, gamma, *F2, s2, e2)
+    e1h, e2h = e1.cpu().numpy(), e2.cpu().numpy()
+    if floor == 0.0:  # a positive floor clamps every state: no error can occur
+        assert (e1h.view(np.uint32) != B.U32_OK).sum() >= nb // 7, "too few error leaves"
+    assert np.array_equal(e1h, e2h)
+    assert same(s1.cpu().numpy(), s2.cpu().numpy())
+    for a, b in zip(F1, F2):
+        assert same(a.cpu().numpy(), b.cpu().numpy())
 
 
 def test_acceptance_c1_hundred_random_subgrids_all_kernels():
