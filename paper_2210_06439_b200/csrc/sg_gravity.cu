@@ -819,6 +819,245 @@ m2l_mirror_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leav
 }
 
 // ---------------------------------------------------------------------------
+// Exact-mode M2L with mirror-paired targets (bit-identical to m2l_kernel).
+// Each thread owns targets x and 7-x (same y, z).  Cluster cx seen from x and
+// cluster 11-cx seen from 7-x share the table entry (|kx|,|ky|,|kz|) and
+// r_x(7-x, 11-cx) == -r_x(x, cx) exactly (small integers + 1/2, times dx:
+// RN is sign-symmetric).  Unlike the FMA mirror kernel the reference's
+// ascending-cx accumulation order must hold for BOTH targets, so the thread
+// loads a row's 12 (inv, inv3, inv5) entries into registers once, then runs
+// two chains in lock step over cx = 0..11: target x uses entry cx, target 7-x
+// uses entry 11-cx -- and both use the SAME cluster crow[cx], so one
+// broadcast cluster load and half a table load serve each pair (2.5 shared
+// loads per pair instead of 5).  Same far/near expression trees as the
+// one-target kernel (compiled.py:394-446).  256 threads = 512 targets.
+// ---------------------------------------------------------------------------
+constexpr int PAIR_THREADS = 256;
+constexpr int PAIR_PITCH = 52;  // 104 words == 8 mod 32: 4 rows x 4 entries of a half-warp tile the banks
+constexpr size_t PAIR_SMEM = sizeof(double) * TAB_N * TAB_N * PAIR_PITCH + sizeof(double2) * NEAR_R * NEAR_R * NEAR_R +
+                             sizeof(double4) * NC * NC * NC + sizeof(double) * NBW * NBW * NBW + sizeof(int) * 32;
+constexpr int64_t PAIR_WORK_PER_CTA = 27 * 4 * 2 * PAIR_THREADS;  // doubles: [slot][comp][target][thread]
+
+// exact far term from register-held table values (compiled.py:399-418, the
+// same expression tree as m2l_far_term)
+template <int ORDER>
+__device__ __forceinline__ void m2l_pair_term(const double4& c, double inv, double inv3, double inv5, double rx,
+                                              double ry, double rz, double& p_f, double& gx_f, double& gy_f,
+                                              double& gz_f) {
+    p_f = -mul(c.x, inv);
+    const double gcom = mul(c.x, inv3);
+    gx_f = -mul(gcom, rx);
+    gy_f = -mul(gcom, ry);
+    gz_f = -mul(gcom, rz);
+    if (ORDER == 1) {
+        const double dr = add(add(mul(c.y, rx), mul(c.z, ry)), mul(c.w, rz));
+        p_f = sub(p_f, mul(dr, inv3));
+        const double t3 = mul(mul(3.0, dr), inv5);
+        gx_f = sub(add(gx_f, mul(c.y, inv3)), mul(t3, rx));
+        gy_f = sub(add(gy_f, mul(c.z, inv3)), mul(t3, ry));
+        gz_f = sub(add(gz_f, mul(c.w, inv3)), mul(t3, rz));
+    }
+}
+
+template <int ORDER>
+__device__ __forceinline__ void m2l_pair_far(const double4& c, double inv, double inv3, double inv5, double rx,
+                                             double ry, double rz, double& ap, double& ax, double& ay, double& az) {
+    double p, gx, gy, gz;
+    m2l_pair_term<ORDER>(c, inv, inv3, inv5, rx, ry, rz, p, gx, gy, gz);
+    ap = add(ap, p);
+    ax = add(ax, gx);
+    ay = add(ay, gy);
+    az = add(az, gz);
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(PAIR_THREADS, 1)
+m2l_pair_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int64_t B, double dx,
+                double rad2, double eps2, FieldView ov, double* __restrict__ work) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* tab = reinterpret_cast<double*>(smem_raw);
+    double2* near_tab = reinterpret_cast<double2*>(tab + TAB_N * TAB_N * PAIR_PITCH);
+    double4* cl = reinterpret_cast<double4*>(near_tab + NEAR_R * NEAR_R * NEAR_R);
+    double* nm = reinterpret_cast<double*>(cl + NC * NC * NC);
+    int* near_slot = reinterpret_cast<int*>(nm + NBW * NBW * NBW);
+    const int tid = threadIdx.x;
+    double* wk = work + (int64_t)blockIdx.x * PAIR_WORK_PER_CTA + tid;
+
+    // far geometry table, identical values to m2l_kernel<.., FAST=false>
+    for (int e = tid; e < TAB_N * TAB_N * TAB_N; e += PAIR_THREADS) {
+        const int ax = e % TAB_N, ay = (e / TAB_N) % TAB_N, az = e / (TAB_N * TAB_N);
+        const double rx = mul(add((double)ax, 0.5), dx);
+        const double ry = mul(add((double)ay, 0.5), dx);
+        const double rz = mul(add((double)az, 0.5), dx);
+        const double r2 = add(add(mul(rx, rx), mul(ry, ry)), mul(rz, rz));
+        double* row = tab + (az * TAB_N + ay) * PAIR_PITCH;
+        if (r2 > rad2) {
+            const double inv = dvd(1.0, dsqrt(add(r2, eps2)));
+            const double inv3 = mul(mul(inv, inv), inv);
+            row[ax] = inv;
+            row[15 + ax] = inv3;
+            row[30 + ax] = mul(mul(inv3, inv), inv);
+        } else {
+            row[ax] = -1.0;
+            row[15 + ax] = 0.0;
+            row[30 + ax] = 0.0;
+        }
+    }
+    for (int e = tid; e < NEAR_R * NEAR_R * NEAR_R; e += PAIR_THREADS) {
+        const int ix = e % NEAR_R, iy = (e / NEAR_R) % NEAR_R, iz = e / (NEAR_R * NEAR_R);
+        const double sx = mul((double)ix, dx), sy = mul((double)iy, dx), sz = mul((double)iz, dx);
+        const double r2s = add(add(mul(sx, sx), mul(sy, sy)), mul(sz, sz));
+        if (r2s > 0.0) {
+            const double invs = dvd(1.0, dsqrt(add(r2s, eps2)));
+            near_tab[e] = make_double2(invs, mul(mul(invs, invs), invs));
+        } else {
+            near_tab[e] = make_double2(-1.0, 0.0);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int k = 0;
+        for (int e = 0; e < 27; ++e) {
+            const int ax = e % 3, ay = (e / 3) % 3, az = e / 9;
+            near_slot[e] = signbit_d(tab[(az * TAB_N + ay) * PAIR_PITCH + ax]) ? k++ : -1;
+        }
+    }
+
+    // warp = one z plane: 4 mirror pairs x 8 rows y
+    const int xa = tid & 3, y = (tid >> 2) & 7, z = tid >> 5;
+    const int xb = 7 - xa;
+    const double txa = (double)xa + 0.5, ty = (double)y + 0.5, tz = (double)z + 0.5;
+    double rxv[NC];
+    int axv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        rxv[c] = mul(sub(txa, add((double)(2 * c - 8), 1.0)), dx);  // compiled.py:394
+        axv[c] = fold(xa - 2 * c + 7);
+    }
+
+    for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+        __syncthreads();
+        {
+            int64_t cx0 = cv.off, cy0 = cv.off, cz0 = cv.off;
+            if (leaves) {
+                cx0 += 4 * (int64_t)leaves[3 * b];
+                cy0 += 4 * (int64_t)leaves[3 * b + 1];
+                cz0 += 4 * (int64_t)leaves[3 * b + 2];
+            }
+            const double4* src = cv.base + b * cv.leaf_stride + cz0 * cv.sz + cy0 * cv.sy + cx0;
+            for (int i = tid; i < 2 * NC * NC * NC; i += PAIR_THREADS) {
+                const int q = i >> 1, cx = q % NC, cy = (q / NC) % NC, cz = q / (NC * NC);
+                const double* s2 = reinterpret_cast<const double*>(src + cz * cv.sz + cy * cv.sy + cx) + 2 * (i & 1);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(reinterpret_cast<double*>(cl) + 2 * i);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(s2) : "memory");
+            }
+        }
+        const double* mc = leaf_origin(mv, leaves, b, 8);
+        for (int i = tid; i < NBW * NBW * NBW; i += PAIR_THREADS) {
+            const int cx = i % NBW, cy = (i / NBW) % NBW, cz = i / (NBW * NBW);
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(nm + i);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                         "l"(mc + (int64_t)(cz + NB0) * mv.sz + (int64_t)(cy + NB0) * mv.sy + (cx + NB0))
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" "cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+        // near-field sums of both targets (same (|kx|,|ky|,|kz|) combos)
+#pragma unroll 1
+        for (int e = 0; e < 27; ++e) {
+            const int k = near_slot[e];
+            if (k < 0) continue;
+            const int ax = e % 3, ay = (e / 3) % 3, az = e / 9;
+            double p, gx, gy, gz;
+            double* w = wk + (k * 8) * PAIR_THREADS;
+            m2l_near_small(nm, near_tab, xa, y, z, cluster_of(xa, ax), cluster_of(y, ay), cluster_of(z, az), dx, p,
+                           gx, gy, gz);
+            w[0] = p;
+            w[PAIR_THREADS] = gx;
+            w[2 * PAIR_THREADS] = gy;
+            w[3 * PAIR_THREADS] = gz;
+            m2l_near_small(nm, near_tab, xb, y, z, cluster_of(xb, ax), cluster_of(y, ay), cluster_of(z, az), dx, p,
+                           gx, gy, gz);
+            w[4 * PAIR_THREADS] = p;
+            w[5 * PAIR_THREADS] = gx;
+            w[6 * PAIR_THREADS] = gy;
+            w[7 * PAIR_THREADS] = gz;
+        }
+        double ap = 0.0, ax_ = 0.0, ay_ = 0.0, az_ = 0.0;
+        double bp = 0.0, bx_ = 0.0, by_ = 0.0, bz_ = 0.0;
+#pragma unroll 1
+        for (int cz = 0; cz < NC; ++cz) {
+            const double rz = mul(sub(tz, add((double)(2 * cz - 8), 1.0)), dx);
+            const int azr = fold(z - 2 * cz + 7);
+#pragma unroll 1
+            for (int cy = 0; cy < NC; ++cy) {
+                const double ry = mul(sub(ty, add((double)(2 * cy - 8), 1.0)), dx);
+                const int ayr = fold(y - 2 * cy + 7);
+                const double* row = tab + (azr * TAB_N + ayr) * PAIR_PITCH;
+                const double4* crow = cl + (cz * NC + cy) * NC;
+                double ti[NC], t3[NC], t5[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    ti[c] = row[axv[c]];
+                    t3[c] = row[15 + axv[c]];
+                    if (ORDER == 1) t5[c] = row[30 + axv[c]];
+                }
+                if (!__any_sync(0xffffffffu, signbit_d(row[0]))) {
+#pragma unroll
+                    for (int cx = 0; cx < NC; ++cx) {
+                        const double4 c = crow[cx];
+                        const int m = NC - 1 - cx;
+                        m2l_pair_far<ORDER>(c, ti[cx], t3[cx], t5[cx], rxv[cx], ry, rz, ap, ax_, ay_, az_);
+                        m2l_pair_far<ORDER>(c, ti[m], t3[m], t5[m], -rxv[m], ry, rz, bp, bx_, by_, bz_);
+                    }
+                } else {
+                    const int rowslot = (azr * 3 + ayr) * 3;
+#pragma unroll
+                    for (int cx = 0; cx < NC; ++cx) {
+                        const double4 c = crow[cx];
+                        const int m = NC - 1 - cx;
+                        double p, gx, gy, gz;
+                        m2l_pair_term<ORDER>(c, ti[cx], t3[cx], t5[cx], rxv[cx], ry, rz, p, gx, gy, gz);
+                        if (signbit_d(ti[cx])) {
+                            const double* w = wk + (near_slot[rowslot + axv[cx]] * 8) * PAIR_THREADS;
+                            p = w[0];
+                            gx = w[PAIR_THREADS];
+                            gy = w[2 * PAIR_THREADS];
+                            gz = w[3 * PAIR_THREADS];
+                        }
+                        ap = add(ap, p);
+                        ax_ = add(ax_, gx);
+                        ay_ = add(ay_, gy);
+                        az_ = add(az_, gz);
+                        m2l_pair_term<ORDER>(c, ti[m], t3[m], t5[m], -rxv[m], ry, rz, p, gx, gy, gz);
+                        if (signbit_d(ti[m])) {
+                            const double* w = wk + (near_slot[rowslot + axv[m]] * 8 + 4) * PAIR_THREADS;
+                            p = w[0];
+                            gx = w[PAIR_THREADS];
+                            gy = w[2 * PAIR_THREADS];
+                            gz = w[3 * PAIR_THREADS];
+                        }
+                        bp = add(bp, p);
+                        bx_ = add(bx_, gx);
+                        by_ = add(by_, gy);
+                        bz_ = add(bz_, gz);
+                    }
+                }
+            }
+        }
+        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy;
+        o[xa] = ap;
+        o[ov.comp_stride + xa] = ax_;
+        o[2 * ov.comp_stride + xa] = ay_;
+        o[3 * ov.comp_stride + xa] = az_;
+        o[xb] = bp;
+        o[ov.comp_stride + xb] = bx_;
+        o[2 * ov.comp_stride + xb] = by_;
+        o[3 * ov.comp_stride + xb] = bz_;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Latency mode for tiny batches ("generate terms in
 // parallel across CTAs, then accumulate serially per target"), used when one
 // leaf per persistent CTA would leave the GPU idle (config 1, the drop-in
@@ -1138,6 +1377,15 @@ int64_t sg_m2l_workspace_bytes(int64_t nleaves) {
     return bytes;
 }
 
+// SG_M2L_ONE_TARGET=1 selects the one-target exact kernel (A/B tooling)
+static bool pair_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SG_M2L_ONE_TARGET");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
            const double* clusters, int64_t cluster_leaf_stride, const int32_t* leaves, int64_t nleaves,
            double dx, double rad2, double eps2, int32_t order, int32_t i0, int32_t i1, double* out,
@@ -1246,6 +1494,18 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
         };
         if (order == 1) go(m2l_mirror_kernel<1>);
         else go(m2l_mirror_kernel<0>);
+        if (full < nleaves) launch_range(full, nleaves - full);
+    } else if (precision == SG_PREC_EXACT && pair_enabled() && small_near && i0 <= 0 && i1 >= 512 && nleaves >= sms) {
+        // exact mode, full rounds: mirror-paired kernel, two ordered chains per thread
+        const int64_t full = nleaves - (2 * rem <= sms ? rem : 0);
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
+            sg_count_launch(1);
+            kern<<<(unsigned)sms, PAIR_THREADS, PAIR_SMEM, (cudaStream_t)stream>>>(mv, cv, leaves, full, dx, rad2,
+                                                                                   eps2, ov, workspace);
+        };
+        if (order == 1) go(m2l_pair_kernel<1>);
+        else go(m2l_pair_kernel<0>);
         if (full < nleaves) launch_range(full, nleaves - full);
     } else if (nleaves > sms && rem > 0 && 2 * rem <= sms) {
         launch_range(0, nleaves - rem);
