@@ -17,6 +17,7 @@
 #include <cmath>
 
 #include <atomic>
+#include <mutex>
 
 #include "sg_common.cuh"
 #include "../../include/sg.h"
@@ -1232,6 +1233,331 @@ m2l_reduce_kernel(const double* __restrict__ terms, const int32_t* __restrict__ 
     o[comp * ov.comp_stride] = acc;
 }
 
+// ---------------------------------------------------------------------------
+// Fused latency mode (1-2 subgrids, small-near regime): one CTA per (leaf, z,
+// y) target row of 8 cells, no global term buffer, no second launch.  15
+// producer warps evaluate the row's terms cluster-row by cluster-row (cz,
+// cy) -- geometry from a per-device cached table, clusters from global/L2 --
+// into a shared-memory ring; one consumer warp runs the 32 ordered chains
+// (8 targets x 4 components) through the ring in the reference's (cz, cy,
+// cx) order (compiled.py:388-446).  The chain of 1728 dependent DADDs per
+// target (~8.2 cycles each on B200, tools/probe/dadd_lat.cu) is the floor;
+// everything else overlaps it.  Terms are the same values m2l_kernel
+// accumulates (same expression trees), so results are bit-identical.
+// ---------------------------------------------------------------------------
+constexpr int FL_RING = 32;         // cluster rows in flight
+constexpr int FL_BATCH = 4;         // rows per consumer readiness check / slot release
+constexpr int FL_ROW = NC * 32;     // doubles per ring slot
+// 16 warps; the consumer is warp 15 (SM sub-partition 3).  The other warps on
+// that sub-partition (3, 7, 11) stay idle so producer issue never competes with
+// the chain; the remaining 12 warps produce.
+constexpr int FL_THREADS = 512;
+constexpr int FL_PRODUCERS = 12;
+constexpr int FL_STAGE = NC + TAB_N;  // double4 per staged row: 12 clusters + 15 table entries
+constexpr size_t FL_SMEM = sizeof(double) * FL_RING * FL_ROW + sizeof(double2) * NEAR_R * NEAR_R * NEAR_R +
+                           sizeof(double4) * FL_PRODUCERS * 2 * FL_STAGE + sizeof(uint64_t) * FL_RING +
+                           sizeof(int) * 4;
+constexpr int64_t FL_MAX_LEAVES = 2;
+
+// the far geometry table of m2l_kernel (same expressions), as
+// {inv, inv3, inv5, 0} per (az, ay, ax) in [0,15)^3
+__global__ void m2l_table_kernel(double dx, double rad2, double eps2, double4* __restrict__ tab) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= TAB_N * TAB_N * TAB_N) return;
+    const int ax = e % TAB_N, ay = (e / TAB_N) % TAB_N, az = e / (TAB_N * TAB_N);
+    const double rx = mul(add((double)ax, 0.5), dx);
+    const double ry = mul(add((double)ay, 0.5), dx);
+    const double rz = mul(add((double)az, 0.5), dx);
+    const double r2 = add(add(mul(rx, rx), mul(ry, ry)), mul(rz, rz));
+    if (r2 > rad2) {
+        const double inv = dvd(1.0, dsqrt(add(r2, eps2)));
+        const double inv3 = mul(mul(inv, inv), inv);
+        tab[e] = make_double4(inv, inv3, mul(mul(inv3, inv), inv), 0.0);
+    } else {
+        tab[e] = make_double4(-1.0, 0.0, 0.0, 0.0);
+    }
+}
+
+// near-field sum of one cluster with masses read from global memory
+// (m2l_near_small's expression tree and order)
+__device__ __forceinline__ void m2l_near_small_g(const double* __restrict__ mc, int64_t msy, int64_t msz,
+                                                 const double2* __restrict__ near_tab, int x, int y, int z, int cx,
+                                                 int cy, int cz, double dx, double& p_n, double& gx_n,
+                                                 double& gy_n, double& gz_n) {
+    p_n = 0.0;
+    gx_n = 0.0;
+    gy_n = 0.0;
+    gz_n = 0.0;
+    const int bxc = 2 * cx - 8, byc = 2 * cy - 8, bzc = 2 * cz - 8;
+    double m[8];
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+        const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+        m[o] = __ldg(mc + (int64_t)(bzc + oz + 8) * msz + (int64_t)(byc + oy + 8) * msy + (bxc + ox + 8));
+    }
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+        const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+        const int si = x - (bxc + ox), sj = y - (byc + oy), sk = z - (bzc + oz);
+        const double2 t = near_tab[(abs(sk) * NEAR_R + abs(sj)) * NEAR_R + abs(si)];
+        const bool ok = !signbit_d(t.x);
+        const double sx = mul((double)si, dx), sy = mul((double)sj, dx), sz = mul((double)sk, dx);
+        const double coms = mul(m[o], t.y);
+        p_n = add(p_n, ok ? -mul(m[o], t.x) : 0.0);
+        gx_n = add(gx_n, ok ? -mul(coms, sx) : 0.0);
+        gy_n = add(gy_n, ok ? -mul(coms, sy) : 0.0);
+        gz_n = add(gz_n, ok ? -mul(coms, sz) : 0.0);
+    }
+}
+
+// intra-CTA flag hand-off (PTX release/acquire at CTA scope, no SC fence)
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v)
+                 : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];\n"
+                 : "=r"(v)
+                 : "r"((unsigned)__cvta_generic_to_shared(p))
+                 : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+                 : "memory");
+}
+// arrive with the default .release.cta semantics (does not wait for cp.async in flight)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared.b64 st, [%0];\n}\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+// non-blocking test of phase `parity` (acquire.cta)
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p)), c = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    return make_double4(a.x, a.y, c.x, c.y);
+}
+
+#ifdef SG_FL_PROBE
+__device__ long long g_fl_probe[256][8];
+#define FL_T(i) (g_fl_probe[blockIdx.x][i] = clock64())
+#else
+#define FL_T(i) ((void)0)
+#endif
+
+template <int ORDER>
+__global__ void __launch_bounds__(FL_THREADS, 1)
+m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, double dx, double eps2,
+                   const double4* __restrict__ gtab, int i0, int i1, FieldView ov) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // ring slot = one cluster row: [cx/2][chain lane][cx&1], chain lane = comp*8 + x,
+    // so the consumer reads two consecutive cx with one 16-byte load
+    double* ring = reinterpret_cast<double*>(smem_raw);
+    double2* near_tab = reinterpret_cast<double2*>(ring + FL_RING * FL_ROW);
+    double4* fl_stage = reinterpret_cast<double4*>(near_tab + NEAR_R * NEAR_R * NEAR_R);
+    uint64_t* full = reinterpret_cast<uint64_t*>(fl_stage + FL_PRODUCERS * 2 * FL_STAGE);
+    int* consumed = reinterpret_cast<int*>(full + FL_RING);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t b = blockIdx.x / 64;
+    const int y = blockIdx.x & 7, z = (blockIdx.x >> 3) & 7;
+    if (tid < FL_RING) mbar_init(full + tid, 1);  // one arrival (the producer's lane 0) per row
+    if (tid == 0) *consumed = 0;
+    for (int e = tid; e < NEAR_R * NEAR_R * NEAR_R; e += FL_THREADS) {
+        const int ix = e % NEAR_R, iy = (e / NEAR_R) % NEAR_R, iz = e / (NEAR_R * NEAR_R);
+        const double sx = mul((double)ix, dx), sy = mul((double)iy, dx), sz = mul((double)iz, dx);
+        const double r2s = add(add(mul(sx, sx), mul(sy, sy)), mul(sz, sz));
+        if (r2s > 0.0) {
+            const double invs = dvd(1.0, dsqrt(add(r2s, eps2)));
+            near_tab[e] = make_double2(invs, mul(mul(invs, invs), invs));
+        } else {
+            near_tab[e] = make_double2(-1.0, 0.0);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) FL_T(0);
+    const double ty = (double)y + 0.5, tz = (double)z + 0.5;
+    if ((warp & 3) == 3 && warp != 15) return;  // idle: shares the consumer's sub-partition
+    if (warp < 15) {
+        const int pw = warp - (warp >> 2);  // producer index 0..11
+        // ---- producers: rows r = pw, pw + 12, ... ; lane -> (x, cx = q, q+4, q+8);
+        // the next row's table entries and clusters are in flight while this one computes
+        const double* mc = leaf_origin(mv, leaves, b, 8);
+        int64_t cx0 = cv.off, cy0 = cv.off, cz0 = cv.off;
+        if (leaves) {
+            cx0 += 4 * (int64_t)leaves[3 * b];
+            cy0 += 4 * (int64_t)leaves[3 * b + 1];
+            cz0 += 4 * (int64_t)leaves[3 * b + 2];
+        }
+        const double4* cbase = cv.base + b * cv.leaf_stride + cz0 * cv.sz + cy0 * cv.sy + cx0;
+        const int x = lane & 7, q = lane >> 3;
+        const double tx = (double)x + 0.5;
+        // per-warp double-buffered staging of a row's 12 clusters and 15 table
+        // entries, filled with cp.async (not register loads: the release fence
+        // on the ready flag would otherwise wait for the prefetch to land)
+        double4* stage = fl_stage + pw * 2 * FL_STAGE;
+        auto load_row = [&](int r, int buf) {
+            if (r < NC * NC) {
+                const int cz = r / NC, cy = r % NC;
+                const double* trow = reinterpret_cast<const double*>(
+                    gtab + (fold(z - 2 * cz + 7) * TAB_N + fold(y - 2 * cy + 7)) * TAB_N);
+                const double* crow = reinterpret_cast<const double*>(cbase + cz * cv.sz + cy * cv.sy);
+                double* dst = reinterpret_cast<double*>(stage + buf * FL_STAGE);
+                for (int c = lane; c < 2 * (NC + TAB_N); c += 32) {
+                    const double* src = c < 2 * NC ? crow + 2 * c : trow + 2 * (c - 2 * NC);
+                    const unsigned d = (unsigned)__cvta_generic_to_shared(dst + 2 * c);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        };
+        load_row(pw, 0);
+        load_row(pw + FL_PRODUCERS, 1);
+#pragma unroll 1
+        for (int r = pw, it = 0; r < NC * NC; r += FL_PRODUCERS, ++it) {
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            __syncwarp();
+            const double4* cst = stage + (it & 1) * FL_STAGE;
+            const double4* tst = cst + NC;
+            const int cz = r / NC, cy = r % NC;
+            const double rz = mul(sub(tz, add((double)(2 * cz - 8), 1.0)), dx);
+            const double ry = mul(sub(ty, add((double)(2 * cy - 8), 1.0)), dx);
+            double p[3], gx[3], gy[3], gz[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int cx = q + 4 * k;
+                const double4 te = tst[fold(x - 2 * cx + 7)];
+                if (!signbit_d(te.x)) {
+                    const double rx = mul(sub(tx, add((double)(2 * cx - 8), 1.0)), dx);
+                    m2l_pair_term<ORDER>(cst[cx], te.x, te.y, te.z, rx, ry, rz, p[k], gx[k], gy[k], gz[k]);
+                } else {
+                    m2l_near_small_g(mc, mv.sy, mv.sz, near_tab, x, y, z, cx, cy, cz, dx, p[k], gx[k], gy[k],
+                                     gz[k]);
+                }
+            }
+            // wait for the ring slot (the consumer has released row r - FL_RING);
+            // warp-uniform spin, every lane acquires
+            while (__any_sync(0xffffffffu, ld_acquire_cta(consumed) <= r - FL_RING)) __nanosleep(32);
+            double* slot = ring + (r % FL_RING) * FL_ROW;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int cx = q + 4 * k;
+                double* s = slot + ((cx >> 1) * 32 + x) * 2 + (cx & 1);
+                s[0] = p[k];
+                s[16] = gx[k];
+                s[32] = gy[k];
+                s[48] = gz[k];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full + r % FL_RING);
+            if (lane == 0 && r == 0) FL_T(1);
+            if (lane == 0 && r == NC * NC - 1) FL_T(2);
+            load_row(r + 2 * FL_PRODUCERS, it & 1);  // this buffer was read above (synced)
+        }
+    } else {
+        // ---- consumer: lane -> (component c = lane >> 3, target x = lane & 7).
+        // Rolling prefetch: the register holding (cx, cx+1) of row r is reloaded
+        // with (cx, cx+1) of row r+1 right after its two adds, so every load has
+        // a full row of the ordered chain (~12 dependent DADDs) to land.
+        // Readiness is tested every FL_BATCH rows (rows r+1 .. r+FL_BATCH), and
+        // slots are handed back with a relaxed store: the adds before it have
+        // consumed every value loaded from them (a release fence would wait on
+        // the prefetches in flight).
+        double acc = 0.0;
+        double2 v[NC / 2];
+        const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * lane;
+        const unsigned cons_s = (unsigned)__cvta_generic_to_shared(consumed);
+        auto ready_rows = [&](int r0) {  // rows r0 .. r0 + FL_BATCH - 1 (< 144) have landed
+            const int rr = r0 + (lane % FL_BATCH);
+            const int rc = rr < NC * NC ? rr : r0;
+            // row r fills slot r % FL_RING for the (r / FL_RING)-th time: phase parity
+            while (__any_sync(0xffffffffu, !mbar_test(full + rc % FL_RING, (rc / FL_RING) & 1))) { }
+        };
+        auto lds2 = [&](unsigned a) {
+            double2 t;
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(t.x), "=d"(t.y) : "r"(a));
+            return t;
+        };
+        ready_rows(0);
+#pragma unroll
+        for (int h = 0; h < NC / 2; ++h) v[h] = lds2(ring_s + 16u * 32u * h);
+        if (lane == 0) FL_T(3);
+#pragma unroll 1
+        for (int r = 0; r < NC * NC; ++r) {
+            if (r % FL_BATCH == 0) ready_rows(r + 1);
+            const bool more = r + 1 < NC * NC;
+            const unsigned nxt = ring_s + 8u * FL_ROW * (unsigned)((r + 1) % FL_RING);
+#pragma unroll
+            for (int h = 0; h < NC / 2; ++h) {
+                acc = add(acc, v[h].x);
+                acc = add(acc, v[h].y);
+                if (more) v[h] = lds2(nxt + 16u * 32u * h);
+            }
+            if (r % FL_BATCH == FL_BATCH - 1 && lane == 0)
+                asm volatile("st.volatile.shared.u32 [%0], %1;\n" ::"r"(cons_s), "r"(r + 1) : "memory");
+        }
+        if (lane == 0) FL_T(5);
+        const int x = lane & 7, c = lane >> 3;
+        const int f = (z * 8 + y) * 8 + x;
+        if (f >= i0 && f < i1) {
+            double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z * ov.sz + y * ov.sy + x;
+            o[c * ov.comp_stride] = acc;
+        }
+    }
+}
+
+// per-device cache of the far geometry table for the latency kernel, keyed
+// by (dx, rad2, eps2); built once on the caller's stream (never evicted:
+// FL_TAB_CAP keys per process, then callers fall back to the two-kernel
+// latency path)
+constexpr int FL_TAB_CAP = 64;
+struct FlTab {
+    int dev;
+    double dx, rad2, eps2;
+    double4* d;
+};
+static std::mutex g_fltab_mu;
+static FlTab g_fltab[FL_TAB_CAP];
+static int g_fltab_n = 0;
+
+static const double4* fl_table(double dx, double rad2, double eps2, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_fltab_mu);
+    for (int i = 0; i < g_fltab_n; ++i) {
+        const FlTab& t = g_fltab[i];
+        if (t.dev == dev && t.dx == dx && t.rad2 == rad2 && t.eps2 == eps2) return t.d;
+    }
+    if (g_fltab_n == FL_TAB_CAP) return nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    double4* d = nullptr;
+    if (cudaMalloc(&d, sizeof(double4) * TAB_N * TAB_N * TAB_N) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    sg_count_launch(1);
+    m2l_table_kernel<<<(TAB_N * TAB_N * TAB_N + 255) / 256, 256, 0, st>>>(dx, rad2, eps2, d);
+    // once per key: make the table visible to every stream that looks it up
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaFree(d);
+        return nullptr;
+    }
+    g_fltab[g_fltab_n++] = FlTab{dev, dx, rad2, eps2, d};
+    return d;
+}
+
 // SM count of the current device, cached per device (atomic: re-entrant)
 static std::atomic<int> g_sm_count[64] = {};
 int sm_count() {
@@ -1377,6 +1703,15 @@ int64_t sg_m2l_workspace_bytes(int64_t nleaves) {
     return bytes;
 }
 
+// SG_M2L_TWO_KERNEL_LATENCY=1 selects the terms + reduce latency path (A/B tooling)
+static bool fused_latency_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SG_M2L_TWO_KERNEL_LATENCY");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 // SG_M2L_ONE_TARGET=1 selects the one-target exact kernel (A/B tooling)
 static bool pair_enabled() {
     static const bool on = [] {
@@ -1463,7 +1798,34 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     // bits do not depend on the launch shape.
     const int64_t sms = sm_count();
     const int64_t rem = nleaves % sms;
-    if (nleaves <= LAT_MAX_LEAVES) {
+    const double4* fltab = nullptr;
+    if (nleaves <= LAT_MAX_LEAVES && small_near && fused_latency_enabled())
+        fltab = fl_table(dx, rad2, eps2, (cudaStream_t)stream);
+    if (fltab) {
+        // fused latency mode: producer warps + one ordered-chain warp per target
+        // row; up to FL_MAX_LEAVES leaves per launch (one 512-thread CTA per SM)
+        for (int64_t first = 0; first < nleaves; first += FL_MAX_LEAVES) {
+            const int64_t count = nleaves - first < FL_MAX_LEAVES ? nleaves - first : FL_MAX_LEAVES;
+            FieldView mvr = mv, ovr = ov;
+            ClusterView cvr = cv;
+            const int32_t* lv = leaves;
+            if (leaves) {
+                lv = leaves + 3 * first;
+            } else {
+                mvr.base += first * mv.leaf_stride;
+                ovr.base += first * ov.leaf_stride;
+                cvr.base += first * cv.leaf_stride;
+            }
+            auto go = [&](auto kern) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FL_SMEM);
+                sg_count_launch(1);
+                kern<<<(unsigned)(count * 64), FL_THREADS, FL_SMEM, (cudaStream_t)stream>>>(mvr, cvr, lv, dx, eps2,
+                                                                                          fltab, i0, i1, ovr);
+            };
+            if (order == 1) go(m2l_latency_kernel<1>);
+            else go(m2l_latency_kernel<0>);
+        }
+    } else if (nleaves <= LAT_MAX_LEAVES) {
         // latency mode (small batches, e.g. one subgrid): terms over
         // nleaves x 12 CTAs, then the ordered per-target reduction
         auto go = [&](auto kern) {

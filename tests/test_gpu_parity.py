@@ -549,10 +549,11 @@ def test_run_steps_public_entry(manifest):
 
 @pytest.mark.parametrize("theta,order", [(0.34, 0), (0.5, 1), (0.2, 1), (0.2, 0)])
 def test_m2l_latency_mode_equals_persistent(theta, order):
-    """Batches of <= 4 subgrids take the two-kernel latency mode (terms over
-    144 CTAs per leaf + ordered reduction); every leaf matches the persistent
-    kernel's bits, near-field regimes (theta 0.2: generic near path) and
-    both expansion orders included."""
+    """Batches of <= 4 subgrids take a latency mode -- the fused producer /
+    ordered-chain kernel in the small-near regime (theta 0.34, 0.5), the
+    terms + ordered-reduction kernels otherwise (theta 0.2: generic near
+    path); every leaf matches the persistent kernel's bits, both expansion
+    orders included."""
     rng = np.random.default_rng(7)
     n, level = 32, 2
     dx = 1.0 / n
@@ -666,3 +667,34 @@ def test_local_slabs_report_first_failing_leaf_in_morton_order():
         four.check_errors(0)
     assert str(got.value) == str(want.value)
     assert "(0, 0, 1)" in str(want.value)
+
+
+def test_m2l_two_kernel_latency_path_in_subprocess():
+    """The fused latency kernel is the default for <= 4 subgrids; the
+    terms + reduce kernels remain the fallback (generic near regime, table
+    cache full, stream capture).  Force them (SG_M2L_TWO_KERNEL_LATENCY=1 is
+    read once per process) and check config 1 against the oracle bitwise."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import oracle as O\n"
+        "from paper_2210_06439_b200 import batched as B, kernels as K, scenarios\n"
+        "from paper_2210_06439_b200.batched import View\n"
+        "dx = 1.0 / 64\n"
+        "cube = scenarios.config1_cube(0)\n"
+        "d = torch.from_numpy(cube).cuda()\n"
+        "cl = torch.empty((12, 12, 12, 4), dtype=torch.float64, device='cuda')\n"
+        "B.cluster_aggregate(d, dx, cl)\n"
+        "for order in (0, 1):\n"
+        "    rad2, eps2 = K.gravity_params(dx, K.GravityConfig(theta=0.34, eps=0.5, expansion_order=order))\n"
+        "    out = torch.zeros((4, 8, 8, 8), dtype=torch.float64, device='cuda')\n"
+        "    B.m2l(d, View(8, 8, 8, 8), cl, 0, None, 1, dx, rad2, eps2, order, out, View(8, 8, 8, 0))\n"
+        "    want = O.multipole(cube, dx, 0.34, 0.5, order)\n"
+        "    assert np.array_equal(out.cpu().numpy().view(np.uint64), want.view(np.uint64)), order\n"
+        "print('ok')\n")
+    env = dict(os.environ, SG_M2L_TWO_KERNEL_LATENCY="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
