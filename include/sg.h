@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SG_ABI_VERSION 3
+#define SG_ABI_VERSION 4
 
 /* precision modes of the gravity kernels:
  *  SG_PREC_EXACT  bit-identical to the reference (no FMA, reference order)
@@ -92,9 +92,13 @@ int sg_p2p(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
  * (near-field partial sums, or for nleaves <= 4 the per-(target, cluster)
  * terms of the latency mode, 28 MB per subgrid; contents are not an output).
  * One workspace per concurrently running call (per stream).  Results are
- * independent of the launch shape: batches of <= 4 subgrids run a term
- * kernel over 144 CTAs per subgrid plus an ordered reduction, larger ones a
- * persistent kernel; both give the same bits. */
+ * independent of the launch shape: batches of <= 4 subgrids run a latency
+ * mode (a fused producer / ordered-chain kernel, 64 CTAs per subgrid, with a
+ * per-device cached geometry table built on first use of a (dx, rad2, eps2)
+ * key -- that first call synchronises `stream` and must not be captured; or,
+ * outside the small-near regime, a term kernel over 144 CTAs per subgrid plus
+ * an ordered reduction), larger ones a persistent kernel (one or two targets
+ * per thread); all give the same bits. */
 int64_t sg_m2l_workspace_bytes(int64_t nleaves);
 int sg_m2l(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
            const double *clusters, int64_t cluster_leaf_stride, const int32_t *leaves, int64_t nleaves,
@@ -189,6 +193,38 @@ int sg_gather_blocks(const double *field, int64_t nx, int64_t ny, int64_t nz, in
  * (pad src_pad) * scale, with scale = dx**3. */
 int sg_scale_copy(double *dst, int32_t dst_pad, const double *src, int32_t src_pad, int64_t nx, int64_t ny,
                   int64_t nz, double scale, void *stream);
+
+/* --------------------------------------------------- per-subgrid drop-in */
+
+/* One SubGrid per call, HOST arrays in and out (the reference's Python entry
+ * points, kernels/__init__.py:122-267, take and fill numpy arrays).  Each
+ * call stages through per-thread pinned and device buffers: one memcpy into
+ * pinned memory, one H2D copy, the batched kernel(s) with nleaves = 1, one
+ * D2H copy and one synchronisation of `stream`.  Same bits as the batched
+ * entry points.  U: (rho, sx, sy, sz, E) stacked (5, 12, 12, 12) blocks with
+ * ghost width 2; out: (phi, gx, gy, gz) interiors as (4, 8, 8, 8). */
+
+/* kernels.max_wavespeed (kernels/__init__.py:264-267). */
+int sg_dropin_max_wavespeed(const double *U, double gamma, double pfloor, double *smax, void *stream);
+/* kernels.monopole_kernel (kernels/__init__.py:205-221): cube = source_cube(sources, "mass", halo),
+ * (8+2*halo)^3. */
+int sg_dropin_monopole(const double *cube, int32_t halo, double dx, double rad2, double eps2, int32_t precision,
+                       double *out, void *stream);
+/* kernels.multipole_prepare + run(i0, i1) (kernels/__init__.py:224-261): cube = source_cube(sources, "mass", 8),
+ * 24^3; clusters are aggregated on the device; only targets [i0, i1) of out are written. */
+int sg_dropin_multipole(const double *cube, double dx, double rad2, double eps2, int32_t order, int32_t i0,
+                        int32_t i1, int32_t precision, double *out, void *stream);
+/* kernels.reconstruct (kernels/__init__.py:122-136): Q is a DEVICE buffer of 5*26*10^3 doubles (it stays on
+ * the device for the following flux call). */
+int sg_dropin_reconstruct(const double *U, double floor_, double *Q, void *stream);
+/* kernels.flux (kernels/__init__.py:150-162): Q, FX, FY, FZ DEVICE buffers; *smax and *err (sg_flux's
+ * status word) returned on the host. */
+int sg_dropin_flux(const double *Q, double gamma, double *FX, double *FY, double *FZ, double *smax, uint32_t *err,
+                   void *stream);
+/* kernels.hydro_update (kernels/__init__.py:165-188) without the CFL check (done by the caller on the host):
+ * U (host, in/out), FX/FY/FZ DEVICE buffers; *status as sg_hydro_update's. */
+int sg_dropin_hydro_update(double *U, const double *FX, const double *FY, const double *FZ, double dt, double dx,
+                           double cfl, uint32_t *status, void *stream);
 
 /* ------------------------------------------------------------ measurement */
 

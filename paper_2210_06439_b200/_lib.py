@@ -10,7 +10,7 @@ import ctypes
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libsg.so"
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -42,6 +42,12 @@ SIGNATURES = {
     "sg_gather_blocks": [_p, _i64, _i64, _i64, _i32, _i64, _p, _i64, _i64, _i32, _p, _p],
     "sg_scale_copy": [_p, _i32, _p, _i32, _i64, _i64, _i64, _d, _p],
     "sg_fp64_peak": [ctypes.c_int, ctypes.c_int, _p, ctypes.POINTER(_i64), _p],
+    "sg_dropin_max_wavespeed": [_p, _d, _d, _p, _p],
+    "sg_dropin_monopole": [_p, _i32, _d, _d, _d, _i32, _p, _p],
+    "sg_dropin_multipole": [_p, _d, _d, _d, _i32, _i32, _i32, _i32, _p, _p],
+    "sg_dropin_reconstruct": [_p, _d, _p, _p],
+    "sg_dropin_flux": [_p, _d, _p, _p, _p, _p, _p, _p],
+    "sg_dropin_hydro_update": [_p, _p, _p, _p, _d, _d, _d, _p, _p],
 }
 
 

@@ -95,6 +95,8 @@ __device__ __forceinline__ bool signbit_d(double v) {
     return __double_as_longlong(v) < 0;
 }
 
+int sm_count();  // SMs of the current device (cached, sg_gravity.cu)
+
 }  // namespace sg
 
 // error reporting shared by every C-ABI entry point

@@ -1618,7 +1618,9 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     FieldView ov = make_view(out, onx, ony, onz, 0, out_leaf_stride);
     const int S = NIN + 2 * halo;
     const int64_t grid = nleaves < 2 * sm_count() ? nleaves : 2 * sm_count();
-    if (halo <= 2) {
+    // batches of a few leaves: one target per thread (p2p_kernel, 512 threads
+    // per leaf) instead of 8 targets per thread on 64 threads per leaf
+    if (halo <= 2 && nleaves * 4 >= sm_count()) {
         // host-built stencil: compiled.py:299-313 with the same IEEE-rounded
         // ops (host code is built with -ffp-contract=off), offsets in
         // (oz, oy, ox) lexicographic order, masked ones dropped

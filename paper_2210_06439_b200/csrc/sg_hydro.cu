@@ -19,10 +19,13 @@
 #include <cstring>
 #include <mutex>
 
+#include <cooperative_groups.h>
+
 #include "sg_common.cuh"
 #include "../../include/sg.h"
 
 namespace sg {
+namespace cg = cooperative_groups;
 
 // geometry.py:21-31: (dz, dy, dx) lexicographic without the zero offset
 __constant__ double c_dirs[NDIR][3];
@@ -149,8 +152,12 @@ reconstruct_kernel(FieldView uv, const int32_t* __restrict__ leaves, double floo
         sl[v][2] = minmod(sub(__ldg(p + uv.sz), u), sub(u, __ldg(p - uv.sz)));
     }
     double* q = Q + b * (int64_t)(NVAR * NDIR * REC_CELLS) + cell;
+    // small batches split the 26 directions over gridDim.z CTAs (the slopes
+    // are recomputed per CTA; every direction's arithmetic is unchanged)
+    const int dper = (NDIR + gridDim.z - 1) / gridDim.z;
+    const int d0 = blockIdx.z * dper, d1 = d0 + dper < NDIR ? d0 + dper : NDIR;
 #pragma unroll 2
-    for (int d = 0; d < NDIR; ++d) {
+    for (int d = d0; d < d1; ++d) {
         const double fdz = c_dirs[d][0], fdy = c_dirs[d][1], fdx = c_dirs[d][2];
         double r[NVAR];
 #pragma unroll
@@ -338,6 +345,51 @@ flux_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX,
         err_out[b] = s_err;
         if (s_err != 0xFFFFFFFFu) latch_error(latch, b, s_err, gate, iter);
     }
+}
+
+// Small batches: each leaf's 1728 faces over a cluster of FLUX_SPLIT CTAs
+// (one face per thread); smax / first-error keys are reduced across the
+// cluster through distributed shared memory into rank 0, which writes them.
+constexpr int FLUX_SPLIT = 3;
+__global__ void __cluster_dims__(FLUX_SPLIT, 1, 1) __launch_bounds__(FLUX_THREADS)
+flux_split_kernel(const double* __restrict__ Q, double gamma, double* __restrict__ FX, double* __restrict__ FY,
+                  double* __restrict__ FZ, double* __restrict__ smax_out, uint32_t* __restrict__ err_out,
+                  uint32_t* __restrict__ latch, int32_t* __restrict__ gate, int32_t iter) {
+    __shared__ unsigned long long s_smax;
+    __shared__ uint32_t s_err;
+    cg::cluster_group cluster = cg::this_cluster();
+    const unsigned rank = cluster.block_rank();
+    const int64_t b = blockIdx.x / FLUX_SPLIT;
+    const int t = threadIdx.x;
+    if (t == 0) {
+        s_smax = 0ull;
+        s_err = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    const double* Qb = Q + b * (int64_t)(NVAR * NDIR * REC_CELLS);
+    const double gm1 = sub(gamma, 1.0);
+    double smax = 0.0;
+    uint32_t err = 0xFFFFFFFFu;
+    int axis, i, j, k;
+    plane_major_face((int)rank * FLUX_THREADS + t, axis, i, j, k);
+    flux_face(Qb, axis, i, j, k, gamma, gm1, b, FX, FY, FZ, smax, err);
+    atomicMax(&s_smax, (unsigned long long)__double_as_longlong(smax));
+    if (err != 0xFFFFFFFFu) atomicMin(&s_err, err);
+    cluster.sync();  // every rank's partials are final (and stay alive for rank 0)
+    if (rank == 0 && t == 0) {
+        unsigned long long m = s_smax;
+        uint32_t e = s_err;
+        for (unsigned r = 1; r < FLUX_SPLIT; ++r) {  // DSMEM reads of the other ranks
+            const unsigned long long mr = *cluster.map_shared_rank(&s_smax, r);
+            const uint32_t er = *cluster.map_shared_rank(&s_err, r);
+            m = mr > m ? mr : m;
+            e = er < e ? er : e;
+        }
+        smax_out[b] = __longlong_as_double((long long)m);
+        err_out[b] = e;
+        if (e != 0xFFFFFFFFu) latch_error(latch, b, e, gate, iter);
+    }
+    cluster.sync();  // keep the partials alive until rank 0 has read them
 }
 
 // ---------------------------------------------------------------------------
@@ -1166,7 +1218,9 @@ int sg_reconstruct(const double* U, int64_t nx, int64_t ny, int64_t nz, int32_t 
         const int32_t* lv = leaves;
         if (leaves) lv += 3 * first;
         else v.base += first * uv.leaf_stride;
-        dim3 grid((REC_CELLS + REC_THREADS - 1) / REC_THREADS, (unsigned)n);
+        // fewer leaves than SMs: spread each leaf's directions over more CTAs
+        const unsigned dsplit = n * 4 >= sm_count() ? 1u : n * 4 * 13 <= 2 * sm_count() ? 13u : 2u;
+        dim3 grid((REC_CELLS + REC_THREADS - 1) / REC_THREADS, (unsigned)n, dsplit);
         sg_count_launch(1);
         reconstruct_kernel<<<grid, REC_THREADS, 0, (cudaStream_t)stream>>>(
             v, lv, floor_, Q + first * (int64_t)(NVAR * NDIR * REC_CELLS));
@@ -1185,8 +1239,13 @@ int sg_flux(const double* Q, int64_t nleaves, double gamma, double* FX, double* 
     SG_TRY(sg_check_ptr("sg_flux", "err", err));
     SG_TRY(init_tables());
     sg_count_launch(1);
-    flux_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax, err, latch,
-                                                                                gate, iter);
+    if (FLUX_SPLIT * nleaves <= sm_count()) {  // latency-bound: one face per thread
+        flux_split_kernel<<<(unsigned)(FLUX_SPLIT * nleaves), FLUX_THREADS, 0, (cudaStream_t)stream>>>(
+            Q, gamma, FX, FY, FZ, smax, err, latch, gate, iter);
+    } else {
+        flux_kernel<<<(unsigned)nleaves, FLUX_THREADS, 0, (cudaStream_t)stream>>>(Q, gamma, FX, FY, FZ, smax, err,
+                                                                                    latch, gate, iter);
+    }
     return sg_check_launch("sg_flux");
 }
 

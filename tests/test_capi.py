@@ -19,7 +19,7 @@ def test_library_exports_every_header_symbol():
     lib = ctypes.CDLL(str(REPO / "paper_2210_06439_b200" / "libsg.so"))
     missing = [s for s in sorted(header_symbols()) if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.sg_abi_version() == 3
+    assert lib.sg_abi_version() == 4
 
 
 def test_binding_table_covers_header():
@@ -113,6 +113,15 @@ def test_argument_validation_without_device():
     bad("sg_gather_blocks", P, 8, 8, 8, 2, 0, N, 1, 1, 2, N, N, match="out is NULL")
     bad("sg_gather_blocks", P, 8, 8, 8, 2, 0, N, 1, 1, 3, P, N, match="halo")
     bad("sg_scale_copy", P, 8, N, 2, 8, 8, 8, 1.0, N, match="src is NULL")
+    # per-subgrid drop-in entry points (host arrays): NULLs are rejected before any CUDA call
+    bad("sg_dropin_max_wavespeed", N, 1.4, 1e-12, P, N, match="U is NULL")
+    bad("sg_dropin_max_wavespeed", P, 1.4, 1e-12, N, N, match="smax is NULL")
+    bad("sg_dropin_monopole", N, 2, d, 1e-3, 1e-5, 0, P, N, match="cube is NULL")
+    bad("sg_dropin_monopole", P, 9, d, 1e-3, 1e-5, 0, P, N, match="halo")
+    bad("sg_dropin_multipole", P, d, 1e-3, 1e-5, 1, 0, 512, 0, N, N, match="out is NULL")
+    bad("sg_dropin_reconstruct", P, 1e-12, N, N, match="Q is NULL")
+    bad("sg_dropin_flux", P, 1.4, P, P, P, P, N, N, match="err is NULL")
+    bad("sg_dropin_hydro_update", N, P, P, P, 1e-3, d, 0.4, P, N, match="U is NULL")
     bad("sg_scale_copy", P, -1, P, 2, 8, 8, 8, 1.0, N, match="negative pad")
     flops = ctypes.c_int64()
     bad("sg_fp64_peak", 3, 1, P, ctypes.byref(flops), N, match="mode")
