@@ -48,7 +48,10 @@ METRIC = "FP64 subgrids/s per kernel (M2L, P2P, hydro) at 1/2/4/8 B200; % FP64/H
 UNIT = "subgrids/s"
 M2L_FLOP = {1: 26_800_128, 0: 8_338_944}      # SURVEY.md §8(d), per subgrid
 P2P_FLOP = 423_936
-HYDRO_ITER_FLOP = 1_174_000 + 1_275_264         # reconstruct + flux
+# fused reconstruct + flux per subgrid: the 512 interior cells
+# reconstruct all 26 directions (1,174 each), the 384 one-layer ring cells only
+# the 9 directions their faces read (30 + 9*44 each), plus the flux's 1,275,264
+HYDRO_ITER_FLOP = 512 * 1_174 + 384 * (30 + 9 * 44) + 1_275_264   # = 2,039,936
 # per-kernel roof and algorithmic work per subgrid: FP64
 # kernels against the measured DADD/DMUL issue rate, HBM kernels against the
 # measured copy bandwidth (update: U interior read + write + the three flux
@@ -325,7 +328,7 @@ def m2l_traffic_from_profile():
         # one section per captured kernel; take the exact M2L one
         for txt in f.read_text().split("== ncu --set full")[1:]:
             name = re.search(r"Kernel Name\s+(.*)", txt)
-            if not name or "m2l_kernel" not in name.group(1):
+            if not name or not ("m2l_kernel" in name.group(1) or "m2l_pair_kernel" in name.group(1)):
                 continue
             vals = {}
             for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):

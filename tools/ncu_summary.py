@@ -8,10 +8,11 @@ import sys
 from collections import Counter
 
 rep = sys.argv[1]
+filt = ["-k", f"regex:{sys.argv[2]}"] if len(sys.argv) > 2 else []
 
 
 def ncu(*a):
-    return subprocess.run(["ncu", "-i", rep, *a], capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", rep, *filt, *a], capture_output=True, text=True).stdout
 
 
 raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
