@@ -218,7 +218,8 @@ def test_bench_roofline_traffic_reads_the_m2l_section():
     traffic, name = bench.m2l_traffic_from_profile()
     assert name is not None and name.endswith("_m2l_L4_ncu_full.txt")
     text = (REPO / "profiles" / name).read_text()
-    sect = [t for t in text.split("== ncu --set full")[1:] if "m2l_kernel" in t.split("\n", 3)[1]]
+    sect = [t for t in text.split("== ncu --set full")[1:]
+            if "m2l_kernel" in t.split("\n", 3)[1] or "m2l_pair_kernel" in t.split("\n", 3)[1]]
     assert sect, name
     assert 1e7 < traffic < 1e9
 
