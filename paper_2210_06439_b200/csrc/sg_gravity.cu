@@ -30,6 +30,8 @@ namespace sg {
 __global__ void cluster_aggregate_kernel(const double* __restrict__ mass, int64_t mnx, int64_t mny,
                                          int64_t ncx, int64_t ncy, int64_t ncz, double dx,
                                          double4* __restrict__ out) {
+    // let a PDL-launched consumer (the latency M2L) start its input-free prologue
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = ncx * ncy * ncz;
     if (i >= total) return;
@@ -1246,7 +1248,7 @@ m2l_reduce_kernel(const double* __restrict__ terms, const int32_t* __restrict__ 
 // accumulates (same expression trees), so results are bit-identical.
 // ---------------------------------------------------------------------------
 constexpr int FL_RING = 32;         // cluster rows in flight
-constexpr int FL_BATCH = 4;         // rows per consumer readiness check / slot release
+constexpr int FL_BATCH = 8;         // rows per consumer readiness check / slot release
 constexpr int FL_ROW = NC * 32;     // doubles per ring slot
 // 16 warps; the consumer is warp 15 (SM sub-partition 3).  The other warps on
 // that sub-partition (3, 7, 11) stay idle so producer issue never competes with
@@ -1385,6 +1387,10 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
             near_tab[e] = make_double2(-1.0, 0.0);
         }
     }
+    // programmatic dependent launch: everything above touches no input; the
+    // inputs (clusters from a preceding sg_cluster_aggregate, masses) are read
+    // only after the previous grid on the stream has completed
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     __syncthreads();
     if (tid == 0) FL_T(0);
     const double ty = (double)y + 0.5, tz = (double)z + 0.5;
@@ -1493,19 +1499,24 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
 #pragma unroll
         for (int h = 0; h < NC / 2; ++h) v[h] = lds2(ring_s + 16u * 32u * h);
         if (lane == 0) FL_T(3);
+        static_assert((NC * NC) % FL_BATCH == 0 && FL_RING % FL_BATCH == 0, "batches tile the rows and the ring");
 #pragma unroll 1
-        for (int r = 0; r < NC * NC; ++r) {
-            if (r % FL_BATCH == 0) ready_rows(r + 1);
-            const bool more = r + 1 < NC * NC;
-            const unsigned nxt = ring_s + 8u * FL_ROW * (unsigned)((r + 1) % FL_RING);
+        for (int rb = 0; rb < NC * NC; rb += FL_BATCH) {
+            ready_rows(rb + 1);
+            const unsigned sb = (unsigned)(rb % FL_RING);
+            const bool last = rb + FL_BATCH == NC * NC;
 #pragma unroll
-            for (int h = 0; h < NC / 2; ++h) {
-                acc = add(acc, v[h].x);
-                acc = add(acc, v[h].y);
-                if (more) v[h] = lds2(nxt + 16u * 32u * h);
+            for (int j = 0; j < FL_BATCH; ++j) {
+                const unsigned nxt = ring_s + 8u * FL_ROW * ((sb + j + 1) % FL_RING);
+#pragma unroll
+                for (int h = 0; h < NC / 2; ++h) {
+                    acc = add(acc, v[h].x);
+                    acc = add(acc, v[h].y);
+                    if (j < FL_BATCH - 1 || !last) v[h] = lds2(nxt + 16u * 32u * h);
+                }
             }
-            if (r % FL_BATCH == FL_BATCH - 1 && lane == 0)
-                asm volatile("st.volatile.shared.u32 [%0], %1;\n" ::"r"(cons_s), "r"(r + 1) : "memory");
+            if (lane == 0)
+                asm volatile("st.volatile.shared.u32 [%0], %1;\n" ::"r"(cons_s), "r"(rb + FL_BATCH) : "memory");
         }
         if (lane == 0) FL_T(5);
         const int x = lane & 7, c = lane >> 3;
@@ -1821,8 +1832,20 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
             auto go = [&](auto kern) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FL_SMEM);
                 sg_count_launch(1);
-                kern<<<(unsigned)(count * 64), FL_THREADS, FL_SMEM, (cudaStream_t)stream>>>(mvr, cvr, lv, dx, eps2,
-                                                                                          fltab, i0, i1, ovr);
+                // PDL: this launch may begin while the previous kernel on the
+                // stream drains; the kernel waits (griddepcontrol.wait) before
+                // reading any input
+                cudaLaunchConfig_t lc = {};
+                lc.gridDim = dim3((unsigned)(count * 64));
+                lc.blockDim = dim3(FL_THREADS);
+                lc.dynamicSmemBytes = FL_SMEM;
+                lc.stream = (cudaStream_t)stream;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                at[0].val.programmaticStreamSerializationAllowed = 1;
+                lc.attrs = at;
+                lc.numAttrs = 1;
+                cudaLaunchKernelEx(&lc, kern, mvr, cvr, lv, dx, eps2, fltab, i0, i1, ovr);
             };
             if (order == 1) go(m2l_latency_kernel<1>);
             else go(m2l_latency_kernel<0>);
