@@ -1258,7 +1258,7 @@ constexpr int FL_PRODUCERS = 12;
 constexpr int FL_STAGE = NC + TAB_N;  // double4 per staged row: 12 clusters + 15 table entries
 constexpr size_t FL_SMEM = sizeof(double) * FL_RING * FL_ROW + sizeof(double2) * NEAR_R * NEAR_R * NEAR_R +
                            sizeof(double4) * FL_PRODUCERS * 2 * FL_STAGE + sizeof(uint64_t) * FL_RING +
-                           sizeof(int) * 4;
+                           sizeof(int) * 4 + sizeof(double) * NBW * NBW * NBW;
 constexpr int64_t FL_MAX_LEAVES = 2;
 
 // the far geometry table of m2l_kernel (same expressions), as
@@ -1277,38 +1277,6 @@ __global__ void m2l_table_kernel(double dx, double rad2, double eps2, double4* _
         tab[e] = make_double4(inv, inv3, mul(mul(inv3, inv), inv), 0.0);
     } else {
         tab[e] = make_double4(-1.0, 0.0, 0.0, 0.0);
-    }
-}
-
-// near-field sum of one cluster with masses read from global memory
-// (m2l_near_small's expression tree and order)
-__device__ __forceinline__ void m2l_near_small_g(const double* __restrict__ mc, int64_t msy, int64_t msz,
-                                                 const double2* __restrict__ near_tab, int x, int y, int z, int cx,
-                                                 int cy, int cz, double dx, double& p_n, double& gx_n,
-                                                 double& gy_n, double& gz_n) {
-    p_n = 0.0;
-    gx_n = 0.0;
-    gy_n = 0.0;
-    gz_n = 0.0;
-    const int bxc = 2 * cx - 8, byc = 2 * cy - 8, bzc = 2 * cz - 8;
-    double m[8];
-#pragma unroll
-    for (int o = 0; o < 8; ++o) {
-        const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
-        m[o] = __ldg(mc + (int64_t)(bzc + oz + 8) * msz + (int64_t)(byc + oy + 8) * msy + (bxc + ox + 8));
-    }
-#pragma unroll
-    for (int o = 0; o < 8; ++o) {
-        const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
-        const int si = x - (bxc + ox), sj = y - (byc + oy), sk = z - (bzc + oz);
-        const double2 t = near_tab[(abs(sk) * NEAR_R + abs(sj)) * NEAR_R + abs(si)];
-        const bool ok = !signbit_d(t.x);
-        const double sx = mul((double)si, dx), sy = mul((double)sj, dx), sz = mul((double)sk, dx);
-        const double coms = mul(m[o], t.y);
-        p_n = add(p_n, ok ? -mul(m[o], t.x) : 0.0);
-        gx_n = add(gx_n, ok ? -mul(coms, sx) : 0.0);
-        gy_n = add(gy_n, ok ? -mul(coms, sy) : 0.0);
-        gz_n = add(gz_n, ok ? -mul(coms, sz) : 0.0);
     }
 }
 
@@ -1371,6 +1339,7 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
     double4* fl_stage = reinterpret_cast<double4*>(near_tab + NEAR_R * NEAR_R * NEAR_R);
     uint64_t* full = reinterpret_cast<uint64_t*>(fl_stage + FL_PRODUCERS * 2 * FL_STAGE);
     int* consumed = reinterpret_cast<int*>(full + FL_RING);
+    double* nm = reinterpret_cast<double*>(consumed + 4);  // near-field masses, cube cells [NB0, NB0+NBW)^3
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t b = blockIdx.x / 64;
     const int y = blockIdx.x & 7, z = (blockIdx.x >> 3) & 7;
@@ -1409,47 +1378,78 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
         const double4* cbase = cv.base + b * cv.leaf_stride + cz0 * cv.sz + cy0 * cv.sy + cx0;
         const int x = lane & 7, q = lane >> 3;
         const double tx = (double)x + 0.5;
+        // Producer pw handles rows r = pw + 12 it, i.e. the fixed cluster row
+        // cy = pw at cz = it: everything that depends only on the lane, cy or
+        // the target row is hoisted (the producers are issue-bound).
+        const int cy = pw;
+        const double ry = mul(sub(ty, add((double)(2 * cy - 8), 1.0)), dx);
+        const int tab_y = fold(y - 2 * cy + 7);
+        double rxk[3];
+        int tek[3], stk[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int cx = q + 4 * k;
+            rxk[k] = mul(sub(tx, add((double)(2 * cx - 8), 1.0)), dx);  // compiled.py:394
+            tek[k] = fold(x - 2 * cx + 7);                                // table entry of (x, cx)
+            stk[k] = ((cx >> 1) * 32 + x) * 2 + (cx & 1);                 // ring offset of (comp 0, x, cx)
+        }
         // per-warp double-buffered staging of a row's 12 clusters and 15 table
-        // entries, filled with cp.async (not register loads: the release fence
-        // on the ready flag would otherwise wait for the prefetch to land)
+        // entries, filled with cp.async (not register loads: the release on the
+        // ready barrier would otherwise wait for the prefetch to land).  Lane
+        // chunks are fixed: c = lane and lane + 32 of the 54 16-byte chunks.
         double4* stage = fl_stage + pw * 2 * FL_STAGE;
-        auto load_row = [&](int r, int buf) {
-            if (r < NC * NC) {
-                const int cz = r / NC, cy = r % NC;
-                const double* trow = reinterpret_cast<const double*>(
-                    gtab + (fold(z - 2 * cz + 7) * TAB_N + fold(y - 2 * cy + 7)) * TAB_N);
-                const double* crow = reinterpret_cast<const double*>(cbase + cz * cv.sz + cy * cv.sy);
-                double* dst = reinterpret_cast<double*>(stage + buf * FL_STAGE);
-                for (int c = lane; c < 2 * (NC + TAB_N); c += 32) {
-                    const double* src = c < 2 * NC ? crow + 2 * c : trow + 2 * (c - 2 * NC);
-                    const unsigned d = (unsigned)__cvta_generic_to_shared(dst + 2 * c);
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
-                }
+        const double* cb = reinterpret_cast<const double*>(cbase + cy * cv.sy);
+        const int64_t cz_step = 4 * cv.sz;  // doubles per cluster z-layer
+        const bool c0_cl = lane < 2 * NC, c1_ok = lane + 32 < 2 * (NC + TAB_N);
+        const int c0_off = c0_cl ? 2 * lane : 2 * (lane - 2 * NC), c1_off = 2 * (lane + 32 - 2 * NC);
+        const unsigned stage_s = (unsigned)__cvta_generic_to_shared(stage) + 16u * lane;
+        auto load_row = [&](int cz, int buf) {
+            if (cz < NC) {
+                const double* trow =
+                    reinterpret_cast<const double*>(gtab + (fold(z - 2 * cz + 7) * TAB_N + tab_y) * TAB_N);
+                const double* crow = cb + cz * cz_step;
+                const unsigned d = stage_s + (unsigned)(buf * FL_STAGE * 32);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d),
+                             "l"(c0_cl ? crow + c0_off : trow + c0_off)
+                             : "memory");
+                if (c1_ok)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 512u), "l"(trow + c1_off)
+                                 : "memory");
             }
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         };
-        load_row(pw, 0);
-        load_row(pw + FL_PRODUCERS, 1);
+        // the near-field masses (read by near rows: an L2 round trip per near
+        // term would stall the ordered chain) are staged once, as the first
+        // cp.async group of every producer; all producers pass a named barrier
+        // after their first wait so every slice is visible
+        for (int i = pw * 32 + lane; i < NBW * NBW * NBW; i += FL_PRODUCERS * 32) {
+            const int ix = i % NBW, iy = (i / NBW) % NBW, iz = i / (NBW * NBW);
+            const unsigned d = (unsigned)__cvta_generic_to_shared(nm + i);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d),
+                         "l"(mc + (int64_t)(iz + NB0) * mv.sz + (int64_t)(iy + NB0) * mv.sy + (ix + NB0))
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        load_row(0, 0);
+        load_row(1, 1);
 #pragma unroll 1
-        for (int r = pw, it = 0; r < NC * NC; r += FL_PRODUCERS, ++it) {
+        for (int cz = 0; cz < NC; ++cz) {
+            const int r = cz * NC + cy;
             asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            if (cz == 0) asm volatile("bar.sync 2, %0;\n" ::"n"(FL_PRODUCERS * 32) : "memory");
             __syncwarp();
-            const double4* cst = stage + (it & 1) * FL_STAGE;
+            const double4* cst = stage + (cz & 1) * FL_STAGE;
             const double4* tst = cst + NC;
-            const int cz = r / NC, cy = r % NC;
             const double rz = mul(sub(tz, add((double)(2 * cz - 8), 1.0)), dx);
-            const double ry = mul(sub(ty, add((double)(2 * cy - 8), 1.0)), dx);
             double p[3], gx[3], gy[3], gz[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const int cx = q + 4 * k;
-                const double4 te = tst[fold(x - 2 * cx + 7)];
+                const double4 te = tst[tek[k]];
                 if (!signbit_d(te.x)) {
-                    const double rx = mul(sub(tx, add((double)(2 * cx - 8), 1.0)), dx);
-                    m2l_pair_term<ORDER>(cst[cx], te.x, te.y, te.z, rx, ry, rz, p[k], gx[k], gy[k], gz[k]);
+                    m2l_pair_term<ORDER>(cst[cx], te.x, te.y, te.z, rxk[k], ry, rz, p[k], gx[k], gy[k], gz[k]);
                 } else {
-                    m2l_near_small_g(mc, mv.sy, mv.sz, near_tab, x, y, z, cx, cy, cz, dx, p[k], gx[k], gy[k],
-                                     gz[k]);
+                    m2l_near_small(nm, near_tab, x, y, z, cx, cy, cz, dx, p[k], gx[k], gy[k], gz[k]);
                 }
             }
             // wait for the ring slot (the consumer has released row r - FL_RING);
@@ -1458,8 +1458,7 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
             double* slot = ring + (r % FL_RING) * FL_ROW;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                const int cx = q + 4 * k;
-                double* s = slot + ((cx >> 1) * 32 + x) * 2 + (cx & 1);
+                double* s = slot + stk[k];
                 s[0] = p[k];
                 s[16] = gx[k];
                 s[32] = gy[k];
@@ -1469,7 +1468,7 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
             if (lane == 0) mbar_arrive(full + r % FL_RING);
             if (lane == 0 && r == 0) FL_T(1);
             if (lane == 0 && r == NC * NC - 1) FL_T(2);
-            load_row(r + 2 * FL_PRODUCERS, it & 1);  // this buffer was read above (synced)
+            load_row(cz + 2, cz & 1);  // this buffer was read above (synced)
         }
     } else {
         // ---- consumer: lane -> (component c = lane >> 3, target x = lane & 7).
