@@ -1418,10 +1418,13 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
             }
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         };
+        load_row(0, 0);
+        load_row(1, 1);
         // the near-field masses (read by near rows: an L2 round trip per near
-        // term would stall the ordered chain) are staged once, as the first
-        // cp.async group of every producer; all producers pass a named barrier
-        // after their first wait so every slice is visible
+        // term would stall the ordered chain) are staged once, as the third
+        // cp.async group of every producer (behind the first two rows, so those
+        // do not wait for it); near clusters only occur in rows cz >= 2, where
+        // all producers pass a named barrier so every slice is visible
         for (int i = pw * 32 + lane; i < NBW * NBW * NBW; i += FL_PRODUCERS * 32) {
             const int ix = i % NBW, iy = (i / NBW) % NBW, iz = i / (NBW * NBW);
             const unsigned d = (unsigned)__cvta_generic_to_shared(nm + i);
@@ -1430,13 +1433,15 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
                          : "memory");
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
-        load_row(0, 0);
-        load_row(1, 1);
 #pragma unroll 1
         for (int cz = 0; cz < NC; ++cz) {
             const int r = cz * NC + cy;
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-            if (cz == 0) asm volatile("bar.sync 2, %0;\n" ::"n"(FL_PRODUCERS * 32) : "memory");
+            if (cz < 2) {  // groups: row 0, row 1, masses, row 2, ...
+                asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+                if (cz == 2) asm volatile("bar.sync 2, %0;\n" ::"n"(FL_PRODUCERS * 32) : "memory");
+            }
             __syncwarp();
             const double4* cst = stage + (cz & 1) * FL_STAGE;
             const double4* tst = cst + NC;
@@ -1454,7 +1459,13 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
             }
             // wait for the ring slot (the consumer has released row r - FL_RING);
             // warp-uniform spin, every lane acquires
+#ifdef SG_FL_PROBE
+            const long long tw = clock64();
+#endif
             while (__any_sync(0xffffffffu, ld_acquire_cta(consumed) <= r - FL_RING)) __nanosleep(32);
+#ifdef SG_FL_PROBE
+            if (pw == 0 && lane == 0) g_fl_probe[blockIdx.x][7] += clock64() - tw;
+#endif
             double* slot = ring + (r % FL_RING) * FL_ROW;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
@@ -1487,7 +1498,13 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
             const int rr = r0 + (lane % FL_BATCH);
             const int rc = rr < NC * NC ? rr : r0;
             // row r fills slot r % FL_RING for the (r / FL_RING)-th time: phase parity
+#ifdef SG_FL_PROBE
+            const long long ts = clock64();
+#endif
             while (__any_sync(0xffffffffu, !mbar_test(full + rc % FL_RING, (rc / FL_RING) & 1))) { }
+#ifdef SG_FL_PROBE
+            if (lane == 0) g_fl_probe[blockIdx.x][6] += clock64() - ts;
+#endif
         };
         auto lds2 = [&](unsigned a) {
             double2 t;

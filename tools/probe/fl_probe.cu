@@ -33,8 +33,11 @@ int main() {
     double a[8] = {0};
     for (int b = 0; b < 64; ++b)
         for (int i = 1; i < 7; ++i) a[i] += (double)(i == 6 ? p[b][6] : p[b][i] - p[b][0]) / 64;
-    printf("cycles after start (avg over 64 CTAs): prod row0 %.0f, prod row143 %.0f, cons row0 %.0f, cons half %.0f, cons end %.0f, cons spin %.0f\n",
+    printf("cycles after start (avg over 64 CTAs): prod row0 %.0f, prod row143 %.0f, cons row0 %.0f, (unused) %.0f, cons end %.0f, cons spin %.0f\n",
            a[1], a[2], a[3], a[4], a[5], a[6]);
+    double sw = 0;
+    for (int b = 0; b < 64; ++b) sw += p[b][7] / 64.0;
+    printf("producer 0 ring-slot wait %.0f cycles (12 rows)\n", sw);
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
