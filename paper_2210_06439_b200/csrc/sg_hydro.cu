@@ -956,6 +956,10 @@ __device__ __forceinline__ void dd_faces(const double* S, int q, int64_t b, doub
     }
 }
 
+#ifdef SG_DD_PROBE
+__device__ long long g_dd_probe[148][4];
+#endif
+
 __global__ void __launch_bounds__(DD_THREADS, 1)
 hydro_dedup_kernel(FieldView uv, const int32_t* __restrict__ leaves, int64_t B, double floor_, double gamma,
                    double* __restrict__ FX, double* __restrict__ FY, double* __restrict__ FZ,
@@ -1002,6 +1006,9 @@ hydro_dedup_kernel(FieldView uv, const int32_t* __restrict__ leaves, int64_t B, 
         const int64_t bn = b + gridDim.x;
 #pragma unroll 1
         for (int p = 0; p < 10; ++p) {
+#ifdef SG_DD_PROBE
+            const long long tx0 = clock64();
+#endif
             // ---- X(p): C(p) (compiled.py:55-72), then the faces of plane p-1
             //      (or, at p = 0, the previous leaf's z-faces (8, 9))
             for (int it = t - 256; it >= 0 && it < 500; it += 256) {  // warps 8-15 (faces on 0-7)
@@ -1029,6 +1036,11 @@ hydro_dedup_kernel(FieldView uv, const int32_t* __restrict__ leaves, int64_t B, 
                 dd_faces(S, p - 1, b, FX, FY, FZ, bad_cur | bad_prev, bad_cur, smax, err);
             }
             __syncthreads();  // C(p) ready; faces of plane p-1 done with S
+#ifdef SG_DD_PROBE
+            const long long tx1 = clock64();
+            if (t == 0) { g_dd_probe[blockIdx.x][0] += tx1 - tx0; }
+            if (t == 0 && p >= 2) g_dd_probe[blockIdx.x][2] += tx1 - tx0;
+#endif
             if (p == 0 && bprev >= 0 && t == 0) {
                 smax_out[bprev] = __longlong_as_double((long long)s_smax);
                 err_out[bprev] = s_err;
@@ -1073,6 +1085,9 @@ hydro_dedup_kernel(FieldView uv, const int32_t* __restrict__ leaves, int64_t B, 
             else asm volatile("cp.async.wait_group 1;\n" ::: "memory");
             bad_prev = bad_cur;
             bad_cur = __syncthreads_or(bad);  // S(p) ready; U planes for C(p+1) landed
+#ifdef SG_DD_PROBE
+            if (t == 0) g_dd_probe[blockIdx.x][1] += clock64() - tx1;
+#endif
         }
         bprev = b;
     }
