@@ -856,6 +856,35 @@ __device__ __forceinline__ void dd_states(const double* __restrict__ Cs, double*
     }
 }
 
+// one distinct state from a cell's preloaded centre / slopes cv[v] = {u,
+// sx, sy, sz}: dd_states' expression tree (compiled.py:74-97, 158-172)
+__device__ __forceinline__ void dd_state_cell(const double (&cv)[NVAR][4], double* __restrict__ S, int d, int x,
+                                              int y, int parity, double floor_, double onepf, double gamma,
+                                              double gm1, int& bad) {
+    const double fdz = c_dirs[d][0], fdy = c_dirs[d][1], fdx = c_dirs[d][2];
+    double r[NVAR];
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v)
+        r[v] = add(cv[v][0], mul(0.5, add(add(mul(fdx, cv[v][1]), mul(fdy, cv[v][2])), mul(fdz, cv[v][3]))));
+    const double rho = r[0] < floor_ ? floor_ : r[0];
+    double en = r[4] < floor_ ? floor_ : r[4];
+    const double sx = r[1], sy = r[2], sz = r[3];
+    const double ke = dvd(mul(0.5, add(add(mul(sx, sx), mul(sy, sy)), mul(sz, sz))), rho);
+    const double emin = add(mul(ke, onepf), floor_);
+    en = en < emin ? emin : en;
+    const double inv = dvd(1.0, rho);
+    const double vx = mul(sx, inv), vy = mul(sy, inv), vz = mul(sz, inv);
+    const double kef = mul(0.5, add(add(mul(sx, vx), mul(sy, vy)), mul(sz, vz)));
+    const double p = mul(gm1, sub(en, kef));
+    const double c = dsqrt(mul(mul(gamma, p), inv));
+    double2* o = reinterpret_cast<double2*>(S) + dd_base(d, parity) + dd_cellpart(x, y);
+    o[0 * DD_NSLOT] = make_double2(rho, inv);
+    o[1 * DD_NSLOT] = make_double2(p, c);
+    o[2 * DD_NSLOT] = make_double2(sx, sy);
+    o[3 * DD_NSLOT] = make_double2(sz, en);
+    if (!(rho > 0.0) || !(p > 0.0)) bad = 1;
+}
+
 // interior state it (0..64*ndir) of directions d0.., cells ordered so a
 // half-warp reads rows y and y+4 of the C array (row pitch 10: 40 == 8 mod
 // 16 doubles, conflict-free)
@@ -1060,25 +1089,37 @@ hydro_dedup_kernel(FieldView uv, const int32_t* __restrict__ leaves, int64_t B, 
             const int par = p & 1;
             int bad = 0;
             {
-                // items: interior cells of the plane's directions (dz = +1 only in
-                // the bottom ring plane 0, dz = -1 only in the top one 9), then
-                // the ring cells
+                // interior cells: one thread per (cell, group of 3-4 directions),
+                // the cell's centre and slopes loaded once and reused by every
+                // direction of its group (26 directions -> 8 groups, the 9 of a
+                // ring plane -> 3); then the ring cells, one state per thread
+                const int ndir = (p == 0 || p == 9) ? 9 : NDIR;
                 const int d0 = p == 0 ? 17 : 0;
-                const int nint = (p == 0 || p == 9) ? 9 * 64 : NDIR * 64;
-                const int nall = (p == 0 || p == 9) ? nint : nint + DD_NRING;
-#pragma unroll 1
-                for (int it = t; it < nall; it += DD_THREADS) {
-                    int d, x, y;
-                    const bool valid = true;
-                    if (it < nint) {
-                        dd_interior_item(it, d0, d, x, y);
-                    } else {
-                        const int e = ring[it - nint];
-                        d = e >> 8;
-                        y = (e >> 4) & 15;
-                        x = e & 15;
+                const int c64 = t & 63, g = t >> 6;
+                if (g < (ndir == 9 ? 3 : 8)) {
+                    int dd, x, y;
+                    dd_interior_item(c64, 0, dd, x, y);
+                    const int cell = y * 10 + x;
+                    double cv[NVAR][4];
+#pragma unroll
+                    for (int v = 0; v < NVAR; ++v)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) cv[v][j] = Cs[v * 400 + j * 100 + cell];
+                    const int n = ndir == 9 ? 3 : 3 + (g < 2);
+                    const int ds = d0 + (ndir == 9 ? 3 * g : 3 * g + (g < 2 ? g : 2));
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (k < n) dd_state_cell(cv, S, ds + k, x, y, par, floor_, onepf, gamma, gm1, bad);
+                }
+                if (p != 0 && p != 9) {
+                    // ring states go to threads 128..415, whose interior group has
+                    // 3 directions (groups 0-1 have 4): at most 4 states per thread
+                    for (int it = t - 128; it >= 0 && it < DD_NRING; it += DD_THREADS) {
+                        const int e = ring[it];
+                        int d = e >> 8, y = (e >> 4) & 15, x = e & 15;
+                        const bool valid = true;
+                        dd_states<1>(Cs, S, &d, &x, &y, &valid, par, floor_, onepf, gamma, gm1, bad);
                     }
-                    dd_states<1>(Cs, S, &d, &x, &y, &valid, par, floor_, onepf, gamma, gm1, bad);
                 }
             }
             if (p == 9) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
