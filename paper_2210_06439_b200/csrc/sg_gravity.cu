@@ -972,7 +972,7 @@ m2l_pair_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves
             if (k < 0) continue;
             const int ax = e % 3, ay = (e / 3) % 3, az = e / 9;
             double p, gx, gy, gz;
-            double* w = wk + (k * 8) * PAIR_THREADS;
+            double* w = wk + (e * 8) * PAIR_THREADS;  // indexed by the combo: no slot lookup in the rows
             m2l_near_small(nm, near_tab, xa, y, z, cluster_of(xa, ax), cluster_of(y, ay), cluster_of(z, az), dx, p,
                            gx, gy, gz);
             w[0] = p;
@@ -1022,7 +1022,7 @@ m2l_pair_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves
                         double p, gx, gy, gz;
                         m2l_pair_term<ORDER>(c, ti[cx], t3[cx], t5[cx], rxv[cx], ry, rz, p, gx, gy, gz);
                         if (signbit_d(ti[cx])) {
-                            const double* w = wk + (near_slot[rowslot + axv[cx]] * 8) * PAIR_THREADS;
+                            const double* w = wk + ((rowslot + axv[cx]) * 8) * PAIR_THREADS;
                             p = w[0];
                             gx = w[PAIR_THREADS];
                             gy = w[2 * PAIR_THREADS];
@@ -1034,7 +1034,7 @@ m2l_pair_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves
                         az_ = add(az_, gz);
                         m2l_pair_term<ORDER>(c, ti[m], t3[m], t5[m], -rxv[m], ry, rz, p, gx, gy, gz);
                         if (signbit_d(ti[m])) {
-                            const double* w = wk + (near_slot[rowslot + axv[m]] * 8 + 4) * PAIR_THREADS;
+                            const double* w = wk + ((rowslot + axv[m]) * 8 + 4) * PAIR_THREADS;
                             p = w[0];
                             gx = w[PAIR_THREADS];
                             gy = w[2 * PAIR_THREADS];
