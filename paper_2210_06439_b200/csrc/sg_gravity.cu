@@ -1015,13 +1015,23 @@ m2l_pair_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves
                     }
                 } else {
                     const int rowslot = (azr * 3 + ayr) * 3;
+                    // A near entry has |kx| - 1/2 = fold(x - 2cx + 7) <= 2 (small-near
+                    // regime); for x = xa in 0..3 that is only cx in 3..6, and for
+                    // the mirror chain (entry 11 - cx) only cx in 5..8: the other
+                    // steps are plain far steps, decided at compile time.
 #pragma unroll
                     for (int cx = 0; cx < NC; ++cx) {
                         const double4 c = crow[cx];
                         const int m = NC - 1 - cx;
+                        const bool a_may = cx >= 3 && cx <= 6, b_may = cx >= 5 && cx <= 8;
+                        if (!a_may && !b_may) {
+                            m2l_pair_far<ORDER>(c, ti[cx], t3[cx], t5[cx], rxv[cx], ry, rz, ap, ax_, ay_, az_);
+                            m2l_pair_far<ORDER>(c, ti[m], t3[m], t5[m], -rxv[m], ry, rz, bp, bx_, by_, bz_);
+                            continue;
+                        }
                         double p, gx, gy, gz;
                         m2l_pair_term<ORDER>(c, ti[cx], t3[cx], t5[cx], rxv[cx], ry, rz, p, gx, gy, gz);
-                        if (signbit_d(ti[cx])) {
+                        if (a_may && signbit_d(ti[cx])) {
                             const double* w = wk + ((rowslot + axv[cx]) * 8) * PAIR_THREADS;
                             p = w[0];
                             gx = w[PAIR_THREADS];
@@ -1033,7 +1043,7 @@ m2l_pair_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves
                         ay_ = add(ay_, gy);
                         az_ = add(az_, gz);
                         m2l_pair_term<ORDER>(c, ti[m], t3[m], t5[m], -rxv[m], ry, rz, p, gx, gy, gz);
-                        if (signbit_d(ti[m])) {
+                        if (b_may && signbit_d(ti[m])) {
                             const double* w = wk + ((rowslot + axv[m]) * 8 + 4) * PAIR_THREADS;
                             p = w[0];
                             gx = w[PAIR_THREADS];
