@@ -753,7 +753,7 @@ m2l_mirror_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leav
             double p, gx, gy, gz;
             m2l_near_small(nm, near_tab, xa, y, z, cluster_of(xa, ax), cluster_of(y, ay), cluster_of(z, az), dx,
                            p, gx, gy, gz);
-            double* w = wk + (k * 8) * MIR_THREADS;
+            double* w = wk + (e * 8) * MIR_THREADS;  // indexed by the combo: no slot lookup in the rows
             w[0] = p;
             w[MIR_THREADS] = gx;
             w[2 * MIR_THREADS] = gy;
@@ -791,11 +791,12 @@ m2l_mirror_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leav
                     for (int cx = 0; cx < NC; ++cx) {
                         const int a = axv[cx];
                         const double inv = row[a], inv3 = row[15 + a], i5 = row[30 + a];
-                        if (!signbit_d(inv)) {
+                        // near entries have |kx| - 1/2 <= 2: only cx in 3..6 for xa in 0..3
+                        if (cx < 3 || cx > 6 || !signbit_d(inv)) {
                             mir_far<ORDER>(crow[cx], inv, inv3, i5, rxv[cx], ry, rz, ap, ax_, ay_, az_);
                             mir_far<ORDER>(crow[NC - 1 - cx], inv, inv3, i5, -rxv[cx], ry, rz, bp, bx_, by_, bz_);
                         } else {
-                            const double* w = wk + (near_slot[rowslot + a] * 8) * MIR_THREADS;
+                            const double* w = wk + ((rowslot + a) * 8) * MIR_THREADS;
                             ap = add(ap, w[0]);
                             ax_ = add(ax_, w[MIR_THREADS]);
                             ay_ = add(ay_, w[2 * MIR_THREADS]);
