@@ -837,8 +837,12 @@ m2l_mirror_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leav
 // one-target kernel (compiled.py:394-446).  256 threads = 512 targets.
 // ---------------------------------------------------------------------------
 constexpr int PAIR_THREADS = 256;
-constexpr int PAIR_PITCH = 52;  // 104 words == 8 mod 32: 4 rows x 4 entries of a half-warp tile the banks
-constexpr size_t PAIR_SMEM = sizeof(double) * TAB_N * TAB_N * PAIR_PITCH + sizeof(double2) * NEAR_R * NEAR_R * NEAR_R +
+// geometry table as (inv, inv3) pairs (one 16-byte load) + inv5: row pitches
+// chosen so a warp's 8 rows x 4 entries hit distinct banks per wavefront
+constexpr int PAIR_P2 = 20;  // double2 per row: 320 B == 64 mod 128
+constexpr int PAIR_P5 = 20;  // doubles per row: 160 B == 32 mod 128
+constexpr size_t PAIR_SMEM = sizeof(double2) * TAB_N * TAB_N * PAIR_P2 + sizeof(double) * TAB_N * TAB_N * PAIR_P5 +
+                             sizeof(double2) * NEAR_R * NEAR_R * NEAR_R +
                              sizeof(double4) * NC * NC * NC + sizeof(double) * NBW * NBW * NBW + sizeof(int) * 32;
 constexpr int64_t PAIR_WORK_PER_CTA = 27 * 4 * 2 * PAIR_THREADS;  // doubles: [slot][comp][target][thread]
 
@@ -879,8 +883,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
 m2l_pair_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, int64_t B, double dx,
                 double rad2, double eps2, FieldView ov, double* __restrict__ work) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* tab = reinterpret_cast<double*>(smem_raw);
-    double2* near_tab = reinterpret_cast<double2*>(tab + TAB_N * TAB_N * PAIR_PITCH);
+    double2* tab2 = reinterpret_cast<double2*>(smem_raw);
+    double* tab5 = reinterpret_cast<double*>(tab2 + TAB_N * TAB_N * PAIR_P2);
+    double2* near_tab = reinterpret_cast<double2*>(tab5 + TAB_N * TAB_N * PAIR_P5);
     double4* cl = reinterpret_cast<double4*>(near_tab + NEAR_R * NEAR_R * NEAR_R);
     double* nm = reinterpret_cast<double*>(cl + NC * NC * NC);
     int* near_slot = reinterpret_cast<int*>(nm + NBW * NBW * NBW);
@@ -894,17 +899,16 @@ m2l_pair_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves
         const double ry = mul(add((double)ay, 0.5), dx);
         const double rz = mul(add((double)az, 0.5), dx);
         const double r2 = add(add(mul(rx, rx), mul(ry, ry)), mul(rz, rz));
-        double* row = tab + (az * TAB_N + ay) * PAIR_PITCH;
+        double2* row2 = tab2 + (az * TAB_N + ay) * PAIR_P2;
+        double* row5 = tab5 + (az * TAB_N + ay) * PAIR_P5;
         if (r2 > rad2) {
             const double inv = dvd(1.0, dsqrt(add(r2, eps2)));
             const double inv3 = mul(mul(inv, inv), inv);
-            row[ax] = inv;
-            row[15 + ax] = inv3;
-            row[30 + ax] = mul(mul(inv3, inv), inv);
+            row2[ax] = make_double2(inv, inv3);
+            row5[ax] = mul(mul(inv3, inv), inv);
         } else {
-            row[ax] = -1.0;
-            row[15 + ax] = 0.0;
-            row[30 + ax] = 0.0;
+            row2[ax] = make_double2(-1.0, 0.0);
+            row5[ax] = 0.0;
         }
     }
     for (int e = tid; e < NEAR_R * NEAR_R * NEAR_R; e += PAIR_THREADS) {
@@ -923,7 +927,7 @@ m2l_pair_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves
         int k = 0;
         for (int e = 0; e < 27; ++e) {
             const int ax = e % 3, ay = (e / 3) % 3, az = e / 9;
-            near_slot[e] = signbit_d(tab[(az * TAB_N + ay) * PAIR_PITCH + ax]) ? k++ : -1;
+            near_slot[e] = signbit_d(tab2[(az * TAB_N + ay) * PAIR_P2 + ax].x) ? k++ : -1;
         }
     }
 
@@ -997,16 +1001,18 @@ m2l_pair_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves
             for (int cy = 0; cy < NC; ++cy) {
                 const double ry = mul(sub(ty, add((double)(2 * cy - 8), 1.0)), dx);
                 const int ayr = fold(y - 2 * cy + 7);
-                const double* row = tab + (azr * TAB_N + ayr) * PAIR_PITCH;
+                const double2* row2 = tab2 + (azr * TAB_N + ayr) * PAIR_P2;
+                const double* row5 = tab5 + (azr * TAB_N + ayr) * PAIR_P5;
                 const double4* crow = cl + (cz * NC + cy) * NC;
                 double ti[NC], t3[NC], t5[NC];
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
-                    ti[c] = row[axv[c]];
-                    t3[c] = row[15 + axv[c]];
-                    if (ORDER == 1) t5[c] = row[30 + axv[c]];
+                    const double2 e2 = row2[axv[c]];
+                    ti[c] = e2.x;
+                    t3[c] = e2.y;
+                    if (ORDER == 1) t5[c] = row5[axv[c]];
                 }
-                if (!__any_sync(0xffffffffu, signbit_d(row[0]))) {
+                if (!__any_sync(0xffffffffu, signbit_d(row2[0].x))) {
 #pragma unroll
                     for (int cx = 0; cx < NC; ++cx) {
                         const double4 c = crow[cx];
