@@ -95,10 +95,13 @@ int sg_p2p(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
  * independent of the launch shape: batches of <= 4 subgrids run a latency
  * mode (a fused producer / ordered-chain kernel, 64 CTAs per subgrid, with a
  * per-device cached geometry table built on first use of a (dx, rad2, eps2)
- * key -- that first call synchronises `stream` and must not be captured; or,
- * outside the small-near regime, a term kernel over 144 CTAs per subgrid plus
- * an ordered reduction), larger ones a persistent kernel (one or two targets
- * per thread); all give the same bits. */
+ * key -- that first call synchronises `stream`; while `stream` is being
+ * captured, or outside the small-near regime, a term kernel over 144 CTAs per
+ * subgrid plus an ordered reduction runs instead).  The fused kernel is
+ * launched with programmatic dependent launch: it may begin while the
+ * previous kernel on `stream` drains and reads no input before that kernel
+ * has completed.  Larger batches run a persistent kernel (two mirror-paired
+ * targets per thread in the exact mode); all give the same bits. */
 int64_t sg_m2l_workspace_bytes(int64_t nleaves);
 int sg_m2l(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, int64_t leaf_stride,
            const double *clusters, int64_t cluster_leaf_stride, const int32_t *leaves, int64_t nleaves,
