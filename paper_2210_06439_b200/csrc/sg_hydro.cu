@@ -916,7 +916,7 @@ __device__ __forceinline__ void dd_face(const double* __restrict__ S, int i, int
     const double2* Rc = S2 + dd_cellpart(xr, yr);
     const int pl_ = zl & 1, pr_ = zr & 1;
     double f[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 1
+#pragma unroll 3  // three quadrature points per iteration: ILP across points (1.23 -> 1.20 ms)
     for (int qp = 0; qp < 9; ++qp) {
         const double w = c_simpson[qp];
         const double2* L = Lc + c_dd_lbase[pl_][AXIS][qp];
