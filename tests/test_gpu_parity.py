@@ -291,6 +291,50 @@ def test_dropin_hydro_chain_stays_on_device():
         K.flux(sub, q, cfg)
 
 
+def test_dropin_hydro_chain_concurrent_threads():
+    """The per-thread native staging (sg_dropin_*) under concurrency: four
+    threads, each on its own stream, run reconstruct -> flux -> max_wavespeed
+    -> hydro_update on their own subgrids (reconstruct returns before its H2D
+    copy has been consumed, so a thread's next call must wait for it before
+    reusing the staging); every result equals the golden bits."""
+    import threading
+
+    g = load_npz("hydro_random.npz")
+    cfg = K.HydroConfig()
+    ids = [i for i in range(6) if (g[f"Uupd{i}"][0] > 0).all() and (g[f"Uupd{i}"][4] > 0).all()]
+    assert ids
+    errors, got = [], {}
+
+    def worker(tid):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                for rep in range(4):
+                    for i in ids:
+                        if (i + rep) % 4 != tid:
+                            continue
+                        sub = _sub_from_block(g[f"U{i}"])
+                        q = K.reconstruct(sub, cfg)
+                        fl = K.flux(sub, q, cfg)
+                        ws = K.max_wavespeed(sub, cfg)
+                        K.hydro_update(sub, fl, g[f"flux_meta{i}"][3], cfg)
+                        got[(i, rep)] = (np.stack([sub.interior(n) for n in octree.HYDRO_FIELDS]), fl.max_speed,
+                                         ws, fl.fx.copy())
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert len(got) == 4 * len(ids)
+    for (i, rep), (u, smax, ws, fx) in got.items():
+        assert bitwise(u, g[f"Uupd{i}"]), (i, rep)
+        assert smax == g[f"flux_meta{i}"][0] and bitwise(fx, g[f"FX{i}"]), (i, rep)
+        assert ws == got[(i, 0)][2]
+
+
 def test_flux_error_first_in_loop_order():
     g = load_npz("hydro_random.npz")
     cfg = K.HydroConfig()
