@@ -299,7 +299,8 @@ def test_dropin_hydro_chain_concurrent_threads():
     reusing the staging); every result equals the golden bits."""
     import threading
 
-    g = load_npz("hydro_random.npz")
+    npz = load_npz("hydro_random.npz")
+    g = {k: npz[k] for k in npz.files}  # materialised: NpzFile is not thread-safe
     cfg = K.HydroConfig()
     ids = [i for i in range(6) if (g[f"Uupd{i}"][0] > 0).all() and (g[f"Uupd{i}"][4] > 0).all()]
     assert ids
