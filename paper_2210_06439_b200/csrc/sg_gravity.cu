@@ -1380,7 +1380,24 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
     __syncthreads();
     if (tid == 0) FL_T(0);
     const double ty = (double)y + 0.5, tz = (double)z + 0.5;
-    if ((warp & 3) == 3 && warp != 15) return;  // idle: shares the consumer's sub-partition
+    if ((warp & 3) == 3 && warp != 15) {
+        // warps 3, 7, 11 share the consumer's sub-partition and run no FP64
+        // work; they stage the near-field masses (read by near rows, cz >= 3:
+        // an L2 round trip per near term would stall the ordered chain) and
+        // signal the producers through named barrier 2 (arrive: no wait)
+        const double* mcn = leaf_origin(mv, leaves, b, 8);
+        const int sw = warp >> 2;  // 0..2
+        for (int i = sw * 32 + lane; i < NBW * NBW * NBW; i += 3 * 32) {
+            const int ix = i % NBW, iy = (i / NBW) % NBW, iz = i / (NBW * NBW);
+            const unsigned d = (unsigned)__cvta_generic_to_shared(nm + i);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d),
+                         "l"(mcn + (int64_t)(iz + NB0) * mv.sz + (int64_t)(iy + NB0) * mv.sy + (ix + NB0))
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" "cp.async.wait_group 0;\n" ::: "memory");
+        asm volatile("bar.arrive 2, %0;\n" ::"n"((FL_PRODUCERS + 3) * 32) : "memory");
+        return;
+    }
     if (warp < 15) {
         const int pw = warp - (warp >> 2);  // producer index 0..11
         // ---- producers: rows r = pw, pw + 12, ... ; lane -> (x, cx = q, q+4, q+8);
@@ -1437,28 +1454,11 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
         };
         load_row(0, 0);
         load_row(1, 1);
-        // the near-field masses (read by near rows: an L2 round trip per near
-        // term would stall the ordered chain) are staged once, as the third
-        // cp.async group of every producer (behind the first two rows, so those
-        // do not wait for it); near clusters only occur in rows cz >= 2, where
-        // all producers pass a named barrier so every slice is visible
-        for (int i = pw * 32 + lane; i < NBW * NBW * NBW; i += FL_PRODUCERS * 32) {
-            const int ix = i % NBW, iy = (i / NBW) % NBW, iz = i / (NBW * NBW);
-            const unsigned d = (unsigned)__cvta_generic_to_shared(nm + i);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d),
-                         "l"(mc + (int64_t)(iz + NB0) * mv.sz + (int64_t)(iy + NB0) * mv.sy + (ix + NB0))
-                         : "memory");
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
 #pragma unroll 1
         for (int cz = 0; cz < NC; ++cz) {
             const int r = cz * NC + cy;
-            if (cz < 2) {  // groups: row 0, row 1, masses, row 2, ...
-                asm volatile("cp.async.wait_group 2;\n" ::: "memory");
-            } else {
-                asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-                if (cz == 2) asm volatile("bar.sync 2, %0;\n" ::"n"(FL_PRODUCERS * 32) : "memory");
-            }
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // groups: row 0, row 1, row 2, ...
+            if (cz == 2) asm volatile("bar.sync 2, %0;\n" ::"n"((FL_PRODUCERS + 3) * 32) : "memory");  // masses in
             __syncwarp();
             const double4* cst = stage + (cz & 1) * FL_STAGE;
             const double4* tst = cst + NC;
