@@ -14,7 +14,11 @@
 // only the data-dependent DADD/DMUL stream.  Masked (+0.0) terms and the
 // unselected far/near branch are skipped: accumulators start at +0.0 and are
 // never -0.0, so skipping x + 0.0 is exact.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cmath>
+#include <cstring>
 
 #include <atomic>
 #include <mutex>
@@ -132,30 +136,88 @@ __device__ int p2p_build_chunk(P2PEntry* ent, int* warp_cnt, int c0, int halo, d
 constexpr int P2P_TPT = 8;
 constexpr int P2P_PARAM_THREADS = 512 / P2P_TPT;
 constexpr int P2P_PARAM_CTAS_PER_SM = 8;
-template <bool FAST>
+// TMA helpers (cp.async.bulk.tensor + mbarrier completion)
+__device__ __forceinline__ void tma_mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_wait(uint64_t* bar, unsigned parity) {
+    for (;;) {
+        unsigned done;
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+    }
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+        "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
+// TMA: the leaf's (8+2h)^3 mass cube arrives as ONE tensor tile copy of
+// box {pitch, S, S} (x rows padded to the conflict-free pitch; the extra
+// columns are neighbours or zero-filled out of bounds) instead of S^3 8-byte
+// cp.async requests; completion on an mbarrier (phase = leaf parity).
+template <bool FAST, bool TMA>
 __global__ void __launch_bounds__(P2P_PARAM_THREADS, P2P_PARAM_CTAS_PER_SM)
 p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, int halo, FieldView ov,
-                 const __grid_constant__ P2PStencil st) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+                 const __grid_constant__ P2PStencil st, const __grid_constant__ CUtensorMap tm) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int S = NIN + 2 * halo;
     const int pitch = p2p_pitch(S);
     const int plane = pitch * S;
     double* const cube = reinterpret_cast<double*>(smem_raw);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(cube + S * plane);
     const int tid = threadIdx.x;
     const int x = tid & 7, y = tid >> 3;
     const double* const col = cube + halo * plane + (y + halo) * pitch + (x + halo);  // target (x, y, 0)
+    if (TMA && tid == 0) tma_mbar_init(bar, 1);
+    unsigned phase = 0;
     for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
-        __syncthreads();  // previous leaf's reads done
-        const double* src = leaf_origin(mv, leaves, b, halo);
-        for (int i = tid; i < S * S * S; i += P2P_PARAM_THREADS) {
-            const int cx = i % S, cy = (i / S) % S, cz = i / (S * S);
-            const unsigned dst = (unsigned)__cvta_generic_to_shared(cube + cz * plane + cy * pitch + cx);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
-                         "l"(src + cz * mv.sz + cy * mv.sy + cx)
-                         : "memory");
+        __syncthreads();  // previous leaf's reads done (and, at the start, the barrier initialised)
+        if (TMA) {
+            if (tid == 0) {
+                // box origin in the tensor (x, y, z): the leaf's interior start minus the halo;
+                // stacked blocks are one taller z extent
+                int64_t cx = mv.pad - halo, cy = mv.pad - halo, cz = mv.pad - halo;
+                if (leaves) {
+                    cx += 8 * (int64_t)leaves[3 * b];
+                    cy += 8 * (int64_t)leaves[3 * b + 1];
+                    cz += 8 * (int64_t)leaves[3 * b + 2];
+                } else {
+                    cz += b * (mv.leaf_stride / mv.sz);
+                }
+                tma_expect_tx(bar, (unsigned)(sizeof(double) * S * plane));
+                tma_load_3d(cube, &tm, (int)cx, (int)cy, (int)cz, bar);
+            }
+            tma_wait(bar, phase);
+            phase ^= 1u;
+        } else {
+            const double* src = leaf_origin(mv, leaves, b, halo);
+            for (int i = tid; i < S * S * S; i += P2P_PARAM_THREADS) {
+                const int cx = i % S, cy = (i / S) % S, cz = i / (S * S);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(cube + cz * plane + cy * pitch + cx);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                             "l"(src + cz * mv.sz + cy * mv.sy + cx)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;\n" "cp.async.wait_group 0;\n" ::: "memory");
+            __syncthreads();
         }
-        asm volatile("cp.async.commit_group;\n" "cp.async.wait_group 0;\n" ::: "memory");
-        __syncthreads();
         double ap[P2P_TPT], ax[P2P_TPT], ay[P2P_TPT], az[P2P_TPT];
 #pragma unroll
         for (int k = 0; k < P2P_TPT; ++k) ap[k] = ax[k] = ay[k] = az[k] = 0.0;
@@ -1602,6 +1664,38 @@ static const double4* fl_table(double dx, double rad2, double eps2, cudaStream_t
     return d;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// 3-D tile map of a padded float64 field (X, Y, Z) for P2P cube boxes
+// {pitch, S, S}; false if the layout is not expressible (TMA needs a 16-byte
+// aligned base and row/plane strides, contiguous stacked blocks)
+static bool p2p_tensor_map(CUtensorMap* tm, const double* base, int64_t X, int64_t Y, int64_t Z, int64_t leaf_stride,
+                           int64_t bx, int64_t by, int64_t bz, int S, int pitch) {
+    auto enc = tensor_map_encoder();
+    if (!enc || (reinterpret_cast<uintptr_t>(base) & 15) || (X * 8) % 16) return false;
+    if (leaf_stride && leaf_stride != bx * by * bz) return false;  // stacked blocks must be contiguous
+    if (S > 256 || pitch > 256 || X > (int64_t)1 << 31 || Z > (int64_t)1 << 31) return false;
+    const cuuint64_t dim[3] = {(cuuint64_t)X, (cuuint64_t)Y, (cuuint64_t)Z};
+    const cuuint64_t str[2] = {(cuuint64_t)(8 * X), (cuuint64_t)(8 * X * Y)};
+    const cuuint32_t box[3] = {(cuuint32_t)pitch, (cuuint32_t)S, (cuuint32_t)S}, one[3] = {1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dim, str, box, one,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // SM count of the current device, cached per device (atomic: re-entrant)
 static std::atomic<int> g_sm_count[64] = {};
 int sm_count() {
@@ -1699,14 +1793,24 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
         const size_t smem = sizeof(double) * (size_t)S * S * p2p_pitch(S);
         const int64_t cap = P2P_PARAM_CTAS_PER_SM * (int64_t)sm_count();
         const int64_t pgrid = nleaves < cap ? nleaves : cap;
+        // tensor map of the mass field (stacked blocks: one taller z extent);
+        // if the layout cannot be described (unaligned base or row stride),
+        // the cp.async staging is used instead
+        CUtensorMap tm;
+        std::memset(&tm, 0, sizeof tm);
+        // (a tile box must start 16-byte aligned in x: pad - halo even, 8-cell leaf steps)
+        const bool tma = ((pad - halo) % 2 == 0) && getenv("SG_P2P_NO_TMA") == nullptr && p2p_tensor_map(&tm, mass, nx + 2 * pad, ny + 2 * pad,
+                                        (nz + 2 * pad) * (leaves ? 1 : nleaves), leaf_stride, nx + 2 * pad, ny + 2 * pad,
+                                        nz + 2 * pad, S, p2p_pitch(S));
+        const size_t smem_t = smem + 16;  // + the mbarrier
         auto go = [&](auto kern) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
             sg_count_launch(1);
-            kern<<<(unsigned)pgrid, P2P_PARAM_THREADS, smem, (cudaStream_t)stream>>>(mv, leaves, nleaves, halo, ov,
-                                                                                     st);
+            kern<<<(unsigned)pgrid, P2P_PARAM_THREADS, smem_t, (cudaStream_t)stream>>>(mv, leaves, nleaves, halo,
+                                                                                       ov, st, tm);
         };
-        if (precision == SG_PREC_FMA) go(p2p_param_kernel<true>);
-        else go(p2p_param_kernel<false>);
+        if (precision == SG_PREC_FMA) tma ? go(p2p_param_kernel<true, true>) : go(p2p_param_kernel<true, false>);
+        else tma ? go(p2p_param_kernel<false, true>) : go(p2p_param_kernel<false, false>);
         return sg_check_launch("sg_p2p");
     }
     const size_t smem = sizeof(P2PEntry) * P2P_THREADS + sizeof(int) * 32 +

@@ -743,3 +743,33 @@ def test_m2l_two_kernel_latency_path_in_subprocess():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("precision", ["exact", "fma"])
+def test_p2p_stacked_blocks_tma_equals_global_field(precision):
+    """sg_p2p over STACKED per-subgrid cubes (leaves == NULL, leaf stride =
+    one (8+2h)^3 block: the tensor map's z extent spans all blocks) equals the
+    same leaves on the padded global field, bit for bit -- both through the
+    TMA-staged kernel (>= 37 subgrids), and both equal to the cp.async path."""
+    level, n = 3, 64
+    dx = 1.0 / n
+    rho = scenarios.config2_rho(1, level)
+    rad2, eps2 = K.gravity_params(dx, K.GravityConfig())
+    mv = View(n, n, n, 8)
+    m = torch.zeros(mv.padded_shape, dtype=torch.float64, device="cuda")
+    m[8:8 + n, 8:8 + n, 8:8 + n] = dev(rho * dx ** 3)
+    B.fill_periodic(m, 1, mv, 7)
+    rng = np.random.default_rng(11)
+    na = n // 8
+    pick = [(int(c) % na, int(c) // na % na, int(c) // (na * na)) for c in rng.permutation(na ** 3)[:80]]
+    leaves = torch.tensor(pick, dtype=torch.int32, device="cuda")
+    out_g = torch.zeros((4, n, n, n), dtype=torch.float64, device="cuda")
+    B.p2p(m, mv, leaves, 80, dx, rad2, eps2, 2, out_g, View(n, n, n, 0), precision=precision)
+    cubes = torch.empty((80, 12, 12, 12), dtype=torch.float64, device="cuda")
+    B.gather_blocks(m, mv, leaves, 80, 1, 2, cubes)
+    out_s = torch.zeros((80, 4, 8, 8, 8), dtype=torch.float64, device="cuda")
+    B.p2p(cubes, View(8, 8, 8, 2, 12 ** 3), None, 80, dx, rad2, eps2, 2, out_s, View(8, 8, 8, 0, 4 * 512),
+          precision=precision)
+    g, st = out_g.cpu().numpy(), out_s.cpu().numpy()
+    for i, (cx, cy, cz) in enumerate(pick):
+        assert bitwise(st[i], g[:, cz * 8:cz * 8 + 8, cy * 8:cy * 8 + 8, cx * 8:cx * 8 + 8]), i
