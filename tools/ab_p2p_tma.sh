@@ -1,5 +1,9 @@
 #!/bin/bash
-# A/B: P2P cube staging by one TMA tile copy vs S^3 cp.async requests
+# A/B: P2P cube staging: double-buffered TMA (default), single-buffer TMA, S^3 cp.async requests
 for L in 4 3; do
-  echo "L=$L tma $(python tools/time_kernels.py $L 7 | python -c 'import json,sys; print(json.load(sys.stdin)["p2p"])') cp.async $(SG_P2P_NO_TMA=1 python tools/time_kernels.py $L 7 | python -c 'import json,sys; print(json.load(sys.stdin)["p2p"])')"
+  for e in "" "SG_P2P_TMA_SINGLE=1" "SG_P2P_NO_TMA=1"; do
+    for prec in exact fma; do
+      echo "L=$L ${e:-tma2} $prec $(env $e python tools/time_kernels.py $L 7 $prec | python -c 'import json,sys; print(json.load(sys.stdin)["p2p"])')"
+    done
+  done
 done
