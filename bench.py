@@ -273,7 +273,7 @@ def run_reference(args) -> None:
     kind = "port-native" if O.use_native() else "port"
     threads = O.max_threads()
     state = scenarios.config5_state(LEVEL)
-    m2l_leaves = max(16 * threads, 64)
+    m2l_leaves = max(48 * threads, 64)
     for _ in range(args.warmup):
         cpu_sample(state, LEVEL, threads, m2l_leaves)
     vals, steps = [], []
@@ -671,7 +671,7 @@ def run_ours(args) -> None:
             from oracle import oracle as O
             kind = "port-native" if O.use_native() else "port"
             threads = O.max_threads()
-            r = cpu_sample(state, LEVEL, threads, max(16 * threads, 64))
+            r = cpu_sample(state, LEVEL, threads, max(48 * threads, 64))
             line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
                                     "build": kind, "sample": r["sample"], "rates": r["rates"],
                                     "extrapolated": True, "sampled_leaves": r["sampled_leaves"],

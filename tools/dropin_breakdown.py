@@ -51,3 +51,19 @@ res = {
     "torch_empty_Q": wall(lambda: torch.empty((5, 26, 10, 10, 10), dtype=torch.float64, device="cuda")),
 }
 print(json.dumps(res))
+
+# flux / reconstruct pieces
+q = K.reconstruct(leaf, h)
+dQ = q.device_values()
+F = torch.empty(3 * 5 * 576, dtype=torch.float64, device="cuda")
+sm, er = ctypes.c_double(), ctypes.c_uint32()
+res2 = {
+    "native_flux_call": wall(lambda: L.sg_dropin_flux(dQ.data_ptr(), 1.4, F.data_ptr(), F.data_ptr() + 8 * 2880,
+                                                      F.data_ptr() + 16 * 2880, ctypes.byref(sm), ctypes.byref(er),
+                                                      st)),
+    "full_flux": wall(lambda: K.flux(leaf, q, h)),
+    "torch_empty_F": wall(lambda: torch.empty(3 * 5 * 576, dtype=torch.float64, device="cuda")),
+    "native_reconstruct_call": wall(lambda: L.sg_dropin_reconstruct(ptr, 1e-12, dQ.data_ptr(), st)),
+    "full_reconstruct": wall(lambda: K.reconstruct(leaf, h)),
+}
+print(json.dumps(res2))

@@ -12,7 +12,7 @@ python bench.py --no-cpu > gpurun_out/bench_plain_$TAG.json 2>&1 && \
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py --no-cpu > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
 python tools/prof_kernels.py gravity 4 > gpurun_out/plain.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"m2l_pair|p2p_param" -s 2 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"m2l_pair|p2p_" -s 2 -c 2 \
     -o gpurun_out/prof_m2l_$TAG -f python tools/prof_kernels.py gravity 4 > gpurun_out/ncu_m2l.log 2>&1; echo "ncu m2l rc=$?"
 python tools/prof_kernels.py gravity 4 fma > gpurun_out/plain.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:m2l_mirror -s 1 -c 1 \
