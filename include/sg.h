@@ -92,12 +92,12 @@ int sg_p2p(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
  * (near-field partial sums, or for nleaves <= 4 the per-(target, cluster)
  * terms of the latency mode, 28 MB per subgrid; contents are not an output).
  * One workspace per concurrently running call (per stream).  Results are
- * independent of the launch shape: batches of <= 4 subgrids run a latency
+ * independent of the launch shape: batches of <= 12 subgrids run a latency
  * mode (a fused producer / ordered-chain kernel, 64 CTAs per subgrid, with a
  * per-device cached geometry table built on first use of a (dx, rad2, eps2)
  * key -- that first call synchronises `stream`; while `stream` is being
- * captured, or outside the small-near regime, a term kernel over 144 CTAs per
- * subgrid plus an ordered reduction runs instead).  The fused kernel is
+ * captured, or outside the small-near regime, batches of <= 4 run a term
+ * kernel over 144 CTAs per subgrid plus an ordered reduction instead).  The fused kernel is
  * launched with programmatic dependent launch: it may begin while the
  * previous kernel on `stream` drains and reads no input before that kernel
  * has completed.  Larger batches run a persistent kernel (two mirror-paired

@@ -1962,6 +1962,18 @@ static bool fused_latency_enabled() {
     return on;
 }
 
+// Largest batch the fused latency kernel takes (FL_MAX_LEAVES per launch,
+// launches chained with PDL): below it the persistent one-target kernel would
+// run 64-128-thread CTAs -- too few warps per SM to hide the DADD latency of
+// the ordered chains.  SG_M2L_FL_BATCH_MAX overrides it (A/B tooling).
+static int64_t fl_batch_max() {
+    static const int64_t v = [] {
+        const char* e = getenv("SG_M2L_FL_BATCH_MAX");
+        return e ? (int64_t)atoll(e) : (int64_t)12;
+    }();
+    return v;
+}
+
 // SG_M2L_ONE_TARGET=1 selects the one-target exact kernel (A/B tooling)
 static bool pair_enabled() {
     static const bool on = [] {
@@ -2049,7 +2061,7 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
     const int64_t sms = sm_count();
     const int64_t rem = nleaves % sms;
     const double4* fltab = nullptr;
-    if (nleaves <= LAT_MAX_LEAVES && small_near && fused_latency_enabled())
+    if (nleaves <= fl_batch_max() && small_near && fused_latency_enabled())
         fltab = fl_table(dx, rad2, eps2, (cudaStream_t)stream);
     if (fltab) {
         // fused latency mode: producer warps + one ordered-chain warp per target

@@ -594,10 +594,10 @@ def test_run_steps_public_entry(manifest):
 
 @pytest.mark.parametrize("theta,order", [(0.34, 0), (0.5, 1), (0.2, 1), (0.2, 0)])
 def test_m2l_latency_mode_equals_persistent(theta, order):
-    """Batches of <= 4 subgrids take a latency mode -- the fused producer /
-    ordered-chain kernel in the small-near regime (theta 0.34, 0.5), the
-    terms + ordered-reduction kernels otherwise (theta 0.2: generic near
-    path); every leaf matches the persistent kernel's bits, both expansion
+    """Small batches take a latency mode -- the fused producer /
+    ordered-chain kernel in the small-near regime (theta 0.34, 0.5; up to 12
+    subgrids), the terms + ordered-reduction kernels otherwise (<= 4;
+    theta 0.2: generic near path) -- and every leaf matches the persistent kernel's bits, both expansion
     orders included."""
     rng = np.random.default_rng(7)
     n, level = 32, 2
@@ -615,7 +615,7 @@ def test_m2l_latency_mode_equals_persistent(theta, order):
     leaves = torch.tensor(allc, dtype=torch.int32, device="cuda")
     B.m2l(mass, mv, cl, 0, leaves, 64, dx, rad2, eps2, order, full, View(n, n, n, 0))
     want = full.cpu().numpy()
-    for count in (1, 3, 4):
+    for count in (1, 3, 4, 6, 8, 12):
         pick = [allc[i] for i in rng.permutation(64)[:count]]
         out = torch.full((4, n, n, n), np.nan, dtype=torch.float64, device="cuda")
         B.m2l(mass, mv, cl, 0, torch.tensor(pick, dtype=torch.int32, device="cuda"), count, dx, rad2, eps2, order,

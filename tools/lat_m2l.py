@@ -19,7 +19,7 @@ u.mass[8:-8, 8:-8, 8:-8] = rho * u.dx ** 3
 u._halo(u.mass, 1, u.mv)
 B.cluster_aggregate(u.mass, u.dx, u.clusters)
 res = {}
-for n in (1, 2, 3, 4, 8, 16, 32):
+for n in (1, 2, 3, 4, 6, 8, 12, 16, 32):
     ts = []
     for _ in range(8):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
