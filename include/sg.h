@@ -93,7 +93,8 @@ int sg_p2p(const double *mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
  * terms of the latency mode, 28 MB per subgrid; contents are not an output).
  * One workspace per concurrently running call (per stream).  Results are
  * independent of the launch shape: batches of <= 12 subgrids run a latency
- * mode (a fused producer / ordered-chain kernel, 64 CTAs per subgrid, with a
+ * mode (a fused producer / ordered-chain kernel, 64 CTAs per subgrid -- 64
+ * two-CTA clusters when a launch carries one subgrid -- with a
  * per-device cached geometry table built on first use of a (dx, rad2, eps2)
  * key -- that first call synchronises `stream`; while `stream` is being
  * captured, or outside the small-near regime, batches of <= 4 run a term

@@ -1397,8 +1397,9 @@ m2l_reduce_kernel(const double* __restrict__ terms, const int32_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// Fused latency mode (1-2 subgrids, small-near regime): one CTA per (leaf, z,
-// y) target row of 8 cells, no global term buffer, no second launch.  15
+// Fused latency mode (1-2 subgrids per launch, small-near regime): one CTA
+// (one subgrid: a two-CTA cluster, see SPLIT) per (leaf, z, y) target row of
+// 8 cells, no global term buffer, no second launch.  12
 // producer warps evaluate the row's terms cluster-row by cluster-row (cz,
 // cy) -- geometry from a per-device cached table, clusters from global/L2 --
 // into a shared-memory ring; one consumer warp runs the 32 ordered chains
@@ -1408,8 +1409,8 @@ m2l_reduce_kernel(const double* __restrict__ terms, const int32_t* __restrict__ 
 // everything else overlaps it.  Terms are the same values m2l_kernel
 // accumulates (same expression trees), so results are bit-identical.
 // ---------------------------------------------------------------------------
-constexpr int FL_RING = 32;         // cluster rows in flight
-constexpr int FL_BATCH = 8;         // rows per consumer readiness check / slot release
+constexpr int FL_RING = 48;         // cluster rows in flight
+constexpr int FL_BATCH = 16;        // rows per consumer readiness check / slot release
 constexpr int FL_ROW = NC * 32;     // doubles per ring slot
 // 16 warps; the consumer is warp 15 (SM sub-partition 3).  The other warps on
 // that sub-partition (3, 7, 11) stay idle so producer issue never competes with
@@ -1476,6 +1477,32 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
     return ok != 0;
 }
 
+// cluster-scope variants for the split latency kernel: the producers of
+// CTA rank 1 write rank 0's ring through distributed shared memory
+__device__ __forceinline__ unsigned cluster_rank0_addr(const void* local) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(local)));
+    return r;
+}
+__device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ unsigned cluster_ctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 __device__ __forceinline__ double4 ldg4(const double4* p) {
     const double2 a = __ldg(reinterpret_cast<const double2*>(p)), c = __ldg(reinterpret_cast<const double2*>(p) + 1);
     return make_double4(a.x, a.y, c.x, c.y);
@@ -1488,7 +1515,12 @@ __device__ long long g_fl_probe[256][8];
 #define FL_T(i) ((void)0)
 #endif
 
-template <int ORDER>
+// SPLIT: one subgrid per launch as 64 two-CTA clusters (128 SMs): rank 0
+// holds the ring and the ordered-chain warp, and the producers of both ranks
+// fill it (rank 0: even cz, rank 1: odd cz; rank 1 through distributed shared
+// memory with cluster-scope release / acquire), doubling the producer issue
+// rate that bounds the single-CTA form.  Same terms, same chain order.
+template <int ORDER, int SPLIT>
 __global__ void __launch_bounds__(FL_THREADS, 1)
 m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ leaves, double dx, double eps2,
                    const double4* __restrict__ gtab, int i0, int i1, FieldView ov) {
@@ -1502,10 +1534,12 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
     int* consumed = reinterpret_cast<int*>(full + FL_RING);
     double* nm = reinterpret_cast<double*>(consumed + 4);  // near-field masses, cube cells [NB0, NB0+NBW)^3
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t b = blockIdx.x / 64;
-    const int y = blockIdx.x & 7, z = (blockIdx.x >> 3) & 7;
-    if (tid < FL_RING) mbar_init(full + tid, 1);  // one arrival (the producer's lane 0) per row
-    if (tid == 0) *consumed = 0;
+    const int rank = SPLIT ? (int)cluster_ctarank() : 0;
+    const int rowid = SPLIT ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int64_t b = rowid / 64;
+    const int y = rowid & 7, z = (rowid >> 3) & 7;
+    if (rank == 0 && tid < FL_RING) mbar_init(full + tid, 1);  // one arrival (the producer's lane 0) per row
+    if (tid == 0) *consumed = 0;  // rank 1: its copy, pushed by rank 0's chain warp
     for (int e = tid; e < NEAR_R * NEAR_R * NEAR_R; e += FL_THREADS) {
         const int ix = e % NEAR_R, iy = (e / NEAR_R) % NEAR_R, iz = e / (NEAR_R * NEAR_R);
         const double sx = mul((double)ix, dx), sy = mul((double)iy, dx), sz = mul((double)iz, dx);
@@ -1520,6 +1554,11 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
     // programmatic dependent launch: everything above touches no input; the
     // inputs (clusters from a preceding sg_cluster_aggregate, masses) are read
     // only after the previous grid on the stream has completed
+    if (SPLIT) {
+        // rank 1 writes rank 0's barriers and ring: they must be initialised
+        if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        cluster_sync_all();
+    }
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     __syncthreads();
     if (tid == 0) FL_T(0);
@@ -1542,8 +1581,16 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
         asm volatile("bar.arrive 2, %0;\n" ::"n"((FL_PRODUCERS + 3) * 32) : "memory");
         return;
     }
+    if (SPLIT && rank == 1 && warp == 15) return;
     if (warp < 15) {
         const int pw = warp - (warp >> 2);  // producer index 0..11
+        constexpr int CZS = SPLIT ? 2 : 1;  // cz stride: the two ranks interleave cz
+        // rank 1: rows are written to a local per-warp double buffer and moved
+        // into rank 0's ring slot by one bulk copy that completes the slot's
+        // mbarrier transaction (no cluster-scope fence on the producer's path)
+        const unsigned ring0 = SPLIT && rank == 1 ? cluster_rank0_addr(ring) : 0u;
+        const unsigned full0 = SPLIT && rank == 1 ? cluster_rank0_addr(full) : 0u;
+        double* xfer = ring + pw * 2 * FL_ROW;  // rank 1 only: its ring is unused
         // ---- producers: rows r = pw, pw + 12, ... ; lane -> (x, cx = q, q+4, q+8);
         // the next row's table entries and clusters are in flight while this one computes
         const double* mc = leaf_origin(mv, leaves, b, 8);
@@ -1596,15 +1643,17 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
             }
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         };
-        load_row(0, 0);
-        load_row(1, 1);
+        const int cz_first = rank;
+        load_row(cz_first, 0);
+        load_row(cz_first + CZS, 1);
 #pragma unroll 1
-        for (int cz = 0; cz < NC; ++cz) {
+        for (int it = 0, cz = cz_first; cz < NC; ++it, cz += CZS) {
             const int r = cz * NC + cy;
             asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // groups: row 0, row 1, row 2, ...
-            if (cz == 2) asm volatile("bar.sync 2, %0;\n" ::"n"((FL_PRODUCERS + 3) * 32) : "memory");  // masses in
+            // masses in before the first row that can hold a near cluster (cz >= 3)
+            if (it == (SPLIT ? 1 : 2)) asm volatile("bar.sync 2, %0;\n" ::"n"((FL_PRODUCERS + 3) * 32) : "memory");
             __syncwarp();
-            const double4* cst = stage + (cz & 1) * FL_STAGE;
+            const double4* cst = stage + (it & 1) * FL_STAGE;
             const double4* tst = cst + NC;
             const double rz = mul(sub(tz, add((double)(2 * cz - 8), 1.0)), dx);
             double p[3], gx[3], gy[3], gz[3];
@@ -1623,25 +1672,60 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
 #ifdef SG_FL_PROBE
             const long long tw = clock64();
 #endif
-            while (__any_sync(0xffffffffu, ld_acquire_cta(consumed) <= r - FL_RING)) __nanosleep(32);
-#ifdef SG_FL_PROBE
-            if (pw == 0 && lane == 0) g_fl_probe[blockIdx.x][7] += clock64() - tw;
-#endif
-            double* slot = ring + (r % FL_RING) * FL_ROW;
+            if (SPLIT && rank == 1) {
+                // the bulk copy issued two rows ago has finished reading this buffer
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+                __syncwarp();
+                double* slot = xfer + (it & 1) * FL_ROW;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                double* s = slot + stk[k];
-                s[0] = p[k];
-                s[16] = gx[k];
-                s[32] = gy[k];
-                s[48] = gz[k];
+                for (int k = 0; k < 3; ++k) {
+                    double* s = slot + stk[k];
+                    s[0] = p[k];
+                    s[16] = gx[k];
+                    s[32] = gy[k];
+                    s[48] = gz[k];
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> bulk copy
+                __syncwarp();
+                // rank 0's slot is free once its chain has consumed row r - FL_RING
+                // (its progress is pushed into this CTA's `consumed`)
+                while (__any_sync(0xffffffffu, ld_acquire_cta(consumed) <= r - FL_RING)) __nanosleep(32);
+#ifdef SG_FL_PROBE
+                if (pw == 0 && lane == 0) g_fl_probe[blockIdx.x][7] += clock64() - tw;
+#endif
+                if (lane == 0) {
+                    const unsigned bar = full0 + 8u * (unsigned)(r % FL_RING);
+                    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(bar),
+                                 "n"(FL_ROW * 8)
+                                 : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                        "cp.async.bulk.commit_group;\n" ::"r"(ring0 + 8u * (unsigned)((r % FL_RING) * FL_ROW)),
+                        "r"((unsigned)__cvta_generic_to_shared(slot)), "n"(FL_ROW * 8), "r"(bar)
+                        : "memory");
+                }
+            } else {
+                while (__any_sync(0xffffffffu, ld_acquire_cta(consumed) <= r - FL_RING)) __nanosleep(32);
+#ifdef SG_FL_PROBE
+                if (pw == 0 && lane == 0) g_fl_probe[blockIdx.x][7] += clock64() - tw;
+#endif
+                double* slot = ring + (r % FL_RING) * FL_ROW;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    double* s = slot + stk[k];
+                    s[0] = p[k];
+                    s[16] = gx[k];
+                    s[32] = gy[k];
+                    s[48] = gz[k];
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full + r % FL_RING);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(full + r % FL_RING);
-            if (lane == 0 && r == 0) FL_T(1);
+            if (lane == 0 && r == rank * NC) FL_T(1);
             if (lane == 0 && r == NC * NC - 1) FL_T(2);
-            load_row(cz + 2, cz & 1);  // this buffer was read above (synced)
+            load_row(cz + 2 * CZS, it & 1);  // this buffer was read above (synced)
         }
+        if (SPLIT && rank == 1 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     } else {
         // ---- consumer: lane -> (component c = lane >> 3, target x = lane & 7).
         // Rolling prefetch: the register holding (cx, cx+1) of row r is reloaded
@@ -1655,6 +1739,8 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
         double2 v[NC / 2];
         const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring) + 16u * lane;
         const unsigned cons_s = (unsigned)__cvta_generic_to_shared(consumed);
+        unsigned cons1 = 0;
+        if (SPLIT) asm volatile("mapa.shared::cluster.u32 %0, %1, 1;\n" : "=r"(cons1) : "r"(cons_s));
         auto ready_rows = [&](int r0) {  // rows r0 .. r0 + FL_BATCH - 1 (< 144) have landed
             const int rr = r0 + (lane % FL_BATCH);
             const int rc = rr < NC * NC ? rr : r0;
@@ -1662,7 +1748,11 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
 #ifdef SG_FL_PROBE
             const long long ts = clock64();
 #endif
-            while (__any_sync(0xffffffffu, !mbar_test(full + rc % FL_RING, (rc / FL_RING) & 1))) { }
+            if (SPLIT) {
+                while (__any_sync(0xffffffffu, !mbar_test_cluster(full + rc % FL_RING, (rc / FL_RING) & 1))) { }
+            } else {
+                while (__any_sync(0xffffffffu, !mbar_test(full + rc % FL_RING, (rc / FL_RING) & 1))) { }
+            }
 #ifdef SG_FL_PROBE
             if (lane == 0) g_fl_probe[blockIdx.x][6] += clock64() - ts;
 #endif
@@ -1692,8 +1782,14 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
                     if (j < FL_BATCH - 1 || !last) v[h] = lds2(nxt + 16u * 32u * h);
                 }
             }
-            if (lane == 0)
+            if (lane == 0) {
                 asm volatile("st.volatile.shared.u32 [%0], %1;\n" ::"r"(cons_s), "r"(rb + FL_BATCH) : "memory");
+                // rank 1's last row (143) needs progress 112; nothing later is
+                // pushed, so no store can reach rank 1 after it has exited
+                if (SPLIT && rb + FL_BATCH <= NC * NC - FL_RING)
+                    asm volatile("st.relaxed.cluster.shared::cluster.u32 [%0], %1;\n" ::"r"(cons1), "r"(rb + FL_BATCH)
+                                 : "memory");
+            }
         }
         if (lane == 0) FL_T(5);
         const int x = lane & 7, c = lane >> 3;
@@ -1974,6 +2070,16 @@ static int64_t fl_batch_max() {
     return v;
 }
 
+// SG_M2L_FL_SPLIT=0 runs single subgrids on one CTA per target row instead
+// of two-CTA clusters (A/B tooling)
+static bool fl_split_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SG_M2L_FL_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // SG_M2L_ONE_TARGET=1 selects the one-target exact kernel (A/B tooling)
 static bool pair_enabled() {
     static const bool on = [] {
@@ -2078,6 +2184,9 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
                 ovr.base += first * ov.leaf_stride;
                 cvr.base += first * cv.leaf_stride;
             }
+            // one subgrid: 64 two-CTA clusters (the second CTA of each adds
+            // producers); two subgrids: 128 single CTAs
+            const bool split = count == 1 && fl_split_enabled();
             auto go = [&](auto kern) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FL_SMEM);
                 sg_count_launch(1);
@@ -2085,19 +2194,28 @@ int sg_m2l(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
                 // stream drains; the kernel waits (griddepcontrol.wait) before
                 // reading any input
                 cudaLaunchConfig_t lc = {};
-                lc.gridDim = dim3((unsigned)(count * 64));
+                lc.gridDim = dim3((unsigned)(count * 64 * (split ? 2 : 1)));
                 lc.blockDim = dim3(FL_THREADS);
                 lc.dynamicSmemBytes = FL_SMEM;
                 lc.stream = (cudaStream_t)stream;
-                cudaLaunchAttribute at[1];
+                cudaLaunchAttribute at[2];
                 at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
                 at[0].val.programmaticStreamSerializationAllowed = 1;
+                at[1].id = cudaLaunchAttributeClusterDimension;
+                at[1].val.clusterDim.x = 2;
+                at[1].val.clusterDim.y = 1;
+                at[1].val.clusterDim.z = 1;
                 lc.attrs = at;
-                lc.numAttrs = 1;
+                lc.numAttrs = split ? 2 : 1;
                 cudaLaunchKernelEx(&lc, kern, mvr, cvr, lv, dx, eps2, fltab, i0, i1, ovr);
             };
-            if (order == 1) go(m2l_latency_kernel<1>);
-            else go(m2l_latency_kernel<0>);
+            if (split) {
+                if (order == 1) go(m2l_latency_kernel<1, 1>);
+                else go(m2l_latency_kernel<0, 1>);
+            } else {
+                if (order == 1) go(m2l_latency_kernel<1, 0>);
+                else go(m2l_latency_kernel<0, 0>);
+            }
         }
     } else if (nleaves <= LAT_MAX_LEAVES) {
         // latency mode (small batches, e.g. one subgrid): terms over

@@ -13,7 +13,7 @@ from paper_2210_06439_b200 import batched as B  # noqa: E402
 from paper_2210_06439_b200 import scenarios  # noqa: E402
 from paper_2210_06439_b200.batched import View  # noqa: E402
 
-reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 40  # events tick at 1.024 us: trimmed mean
 cube = torch.from_numpy(scenarios.config1_cube(0)).cuda()
 cl = torch.empty((12, 12, 12, 4), dtype=torch.float64, device="cuda")
 res = torch.empty((4, 8, 8, 8), dtype=torch.float64, device="cuda")
@@ -39,5 +39,6 @@ for busy in (True, False):
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e3)
-    out["busy" if busy else "idle"] = round(statistics.median(ts[1:]), 2)
+    ts = sorted(ts[1:])[reps // 10:reps - reps // 10]
+    out["busy" if busy else "idle"] = round(statistics.mean(ts), 2)
 print(json.dumps({"config1_us": out}))

@@ -1,5 +1,7 @@
-"""M2L device time (host launch cost hidden) vs batch size on the level-3 config-3 grid (CUDA events,
-median of reps): shows the latency-mode / persistent-kernel crossover."""
+"""M2L device time (host launch cost hidden) vs batch size on the level-3 config-3 grid: shows the
+latency-mode / persistent-kernel crossover.  CUDA event timestamps on the B200 boxes tick every
+1.024 us, so each batch size reports the 10%-trimmed mean of 40 reps (the busy-GPU sleep before
+each rep dithers the phase), not a median of quantised values."""
 import json
 import statistics
 import sys
@@ -21,7 +23,7 @@ B.cluster_aggregate(u.mass, u.dx, u.clusters)
 res = {}
 for n in (1, 2, 3, 4, 6, 8, 12, 16, 32):
     ts = []
-    for _ in range(8):
+    for _ in range(42):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda._sleep(200000)  # keep the GPU busy so host launch cost is not timed
         a.record()
@@ -29,5 +31,6 @@ for n in (1, 2, 3, 4, 6, 8, 12, 16, 32):
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e3)
-    res[n] = round(statistics.median(ts[2:]), 1)
+    ts = sorted(ts[2:])[4:-4]
+    res[n] = round(statistics.mean(ts), 2)
 print(json.dumps({"precision": prec, "m2l_us_by_batch": res}))

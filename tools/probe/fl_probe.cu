@@ -4,7 +4,9 @@
 #include "../../paper_2210_06439_b200/csrc/sg_gravity.cu"
 #include <cstdio>
 #include <vector>
-int main() {
+int main(int argc, char** argv) {
+    // argv[1] = CTA stride of the consumer CTAs (2 under SG_M2L_FL_SPLIT=1/2: rank 0 = even CTAs)
+    const int cs = argc > 1 ? atoi(argv[1]) : 1;
     const int n = 24;
     std::vector<double> h(n * n * n);
     for (int i = 0; i < n * n * n; ++i) h[i] = 1.0 + (i % 7) * 0.1;
@@ -31,13 +33,23 @@ int main() {
     long long p[256][8];
     cudaMemcpyFromSymbol(p, g_fl_probe, sizeof p);
     double a[8] = {0};
-    for (int b = 0; b < 64; ++b)
+    for (int b = 0; b < 64 * cs; b += cs)
         for (int i = 1; i < 7; ++i) a[i] += (double)(i == 6 ? p[b][6] : p[b][i] - p[b][0]) / 64;
     printf("cycles after start (avg over 64 CTAs): prod row0 %.0f, prod row143 %.0f, cons row0 %.0f, (unused) %.0f, cons end %.0f, cons spin %.0f\n",
            a[1], a[2], a[3], a[4], a[5], a[6]);
     double sw = 0;
-    for (int b = 0; b < 64; ++b) sw += p[b][7] / 64.0;
+    for (int b = 0; b < 64 * cs; b += cs) sw += p[b][7] / 64.0;
     printf("producer 0 ring-slot wait %.0f cycles (12 rows)\n", sw);
+    if (cs == 2) {  // rank-1 CTAs: producers of the odd cz planes
+        double r143 = 0, w1 = 0, r1 = 0;
+        for (int b = 1; b < 128; b += 2) {
+            r143 += (double)(p[b][2] - p[b - 1][0]) / 64;
+            r1 += (double)(p[b][1] - p[b - 1][0]) / 64;
+            w1 += p[b][7] / 64.0;
+        }
+        printf("rank 1: first row issued %.0f, row 143 issued %.0f cycles after rank 0's start; producer 0 wait %.0f\n",
+               r1, r143, w1);
+    }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
