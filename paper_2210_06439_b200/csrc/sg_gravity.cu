@@ -1484,16 +1484,6 @@ __device__ __forceinline__ unsigned cluster_rank0_addr(const void* local) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(local)));
     return r;
 }
-__device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, unsigned parity) {
-    unsigned ok;
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
 __device__ __forceinline__ unsigned cluster_ctarank() {
     unsigned r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -1748,11 +1738,9 @@ m2l_latency_kernel(FieldView mv, ClusterView cv, const int32_t* __restrict__ lea
 #ifdef SG_FL_PROBE
             const long long ts = clock64();
 #endif
-            if (SPLIT) {
-                while (__any_sync(0xffffffffu, !mbar_test_cluster(full + rc % FL_RING, (rc / FL_RING) & 1))) { }
-            } else {
-                while (__any_sync(0xffffffffu, !mbar_test(full + rc % FL_RING, (rc / FL_RING) & 1))) { }
-            }
+            // (CTA-scope acquire also covers the rank-1 rows: their bytes land by
+            // bulk copies whose completion is this barrier's transaction count)
+            while (__any_sync(0xffffffffu, !mbar_test(full + rc % FL_RING, (rc / FL_RING) & 1))) { }
 #ifdef SG_FL_PROBE
             if (lane == 0) g_fl_probe[blockIdx.x][6] += clock64() - ts;
 #endif
