@@ -48,6 +48,37 @@ def test_m2l_p2p_random_cubes(dx, theta, eps, order):
     assert same(out.cpu().numpy(), O.monopole(sub, dx, theta, eps))
 
 
+@pytest.mark.parametrize("nb,dx", [(64, 1.0 / 64), (2400, 1.0 / 128), (64, 0.1)])
+def test_p2p_batched_edge_masses_vs_oracle(nb, dx):
+    """Batched P2P (the persistent stencil kernels: 64 subgrids take the
+    single-buffer TMA kernel, 2400 the double-buffered one) bitwise against
+    the oracle per subgrid, with cubes aimed at the exact K8 shortcut's
+    guards: zeros (+/-), NaN, inf, subnormal and huge masses, masses at the
+    edges of the shortcut's exponent range; dx = 0.1 (not a power of two)
+    must take the plain 9-op loop."""
+    rng = np.random.default_rng(nb)
+    cubes = rng.lognormal(0.0, 1.0, (nb, 12, 12, 12)) * dx ** 3
+    special = [np.nan, np.inf, -np.inf, 5e-324, 2.0 ** -1030, 2.0 ** -900, 2.0 ** -700, 2.0 ** 700,
+               2.0 ** 900, 1e308, -0.0, 0.0]
+    checked = list(range(0, nb, max(1, nb // 40)))
+    for j, i in enumerate(checked):
+        k = j % (len(special) + 4)
+        if k < len(special):
+            cubes[i, rng.integers(0, 12), rng.integers(0, 12), rng.integers(0, 12)] = special[k]
+        elif k == len(special):
+            cubes[i] *= -1.0                                   # negative masses
+        elif k == len(special) + 1:
+            cubes[i][rng.uniform(size=(12, 12, 12)) < 0.3] = -0.0
+    d = torch.from_numpy(cubes).cuda()
+    cfg = K.GravityConfig(theta=0.34, eps=0.5)
+    rad2, eps2 = K.gravity_params(dx, cfg)
+    out = torch.zeros((nb, 4, 8, 8, 8), dtype=torch.float64, device="cuda")
+    B.p2p(d, View(8, 8, 8, 2, 12 ** 3), None, nb, dx, rad2, eps2, 2, out, View(8, 8, 8, 0, 4 * 512))
+    got = out.cpu().numpy()
+    for i in checked:
+        assert same(got[i], O.monopole(cubes[i], dx, 0.34, 0.5)), i
+
+
 def test_m2l_nan_and_inf_masses_propagate_like_reference():
     rng = np.random.default_rng(9)
     cube = rng.lognormal(0.0, 1.0, (24, 24, 24))
@@ -105,6 +136,64 @@ def test_hydro_random_blocks(gamma, floor, seed):
     assert same(FX2.cpu().numpy(), FXh) and same(FY2.cpu().numpy(), FYh) and same(FZ2.cpu().numpy(), FZh)
     assert same(smax2.cpu().numpy(), smax.cpu().numpy())
     assert np.array_equal(err2.cpu().numpy(), err.cpu().numpy())
+
+
+def _edge_blocks(gamma):
+    """Hydro blocks aimed at the fused kernel's exact shortcuts (direction
+    folding, shared-reciprocal kinetic energy): -0.0 centre values under
+    zero slopes (the zero-sum sign reaches u + 0.5*sum), +0.0 momenta,
+    infinite slopes, and magnitudes outside 2^+-500 / subnormal."""
+    rng = np.random.default_rng(77)
+    out = []
+    for kind in range(8):
+        rho = 1.0 + 0.5 * rng.uniform(-1, 1, (12, 12, 12))
+        v = rng.uniform(-1, 1, (3, 12, 12, 12))
+        p = 1.0 + 0.5 * rng.uniform(-1, 1, (12, 12, 12))
+        U = np.stack([rho, rho * v[0], rho * v[1], rho * v[2], p / (gamma - 1.0) + 0.5 * rho * (v ** 2).sum(0)])
+        if kind == 0:                     # uniform state, momenta all -0.0
+            U[0], U[4] = 1.0, 2.5
+            U[1:4] = -0.0
+        elif kind == 1:                   # -0.0 momenta in a constant patch, random elsewhere
+            U[:, 3:9, 3:9, 3:9] = np.array([1.0, -0.0, -0.0, -0.0, 2.5])[:, None, None, None]
+        elif kind == 2:                   # mixed +0.0 / -0.0 momenta on a uniform background
+            U[0], U[4] = 1.0, 2.5
+            U[1:4] = np.where(rng.uniform(size=(3, 12, 12, 12)) < 0.5, 0.0, -0.0)
+        elif kind == 3:                   # an infinite energy: infinite slopes around it
+            U[4, 6, 5, 6] = np.inf
+        elif kind == 4:                   # huge scale: exponents beyond 2^500
+            U *= 2.0 ** 700
+        elif kind == 5:                   # tiny scale: beyond 2^-500
+            U *= 2.0 ** -700
+        elif kind == 6:                   # subnormal momenta
+            U[1:4] *= 2.0 ** -1070
+        elif kind == 7:                   # -0.0 densities and energies in a uniform patch
+            U[:, 2:6, 2:6, 2:6] = np.array([-0.0, 0.3, -0.0, 0.1, -0.0])[:, None, None, None]
+        out.append(U)
+    return np.stack(out)
+
+
+@pytest.mark.parametrize("floor", [0.0, 1e-12])
+def test_fused_hydro_edge_values_vs_oracle(floor):
+    """The deduplicated fused kernel bitwise against the oracle on the edge
+    blocks (fluxes, smax, first-error word)."""
+    gamma = 1.4
+    U = _edge_blocks(gamma)
+    nb = len(U)
+    Ud = torch.from_numpy(U).cuda()
+    v = View(8, 8, 8, 2, leaf_stride=5 * 1728)
+    shp = dict(dtype=torch.float64, device="cuda")
+    F = [torch.empty((nb, 5, 8, 8, 9), **shp), torch.empty((nb, 5, 8, 9, 8), **shp),
+         torch.empty((nb, 5, 9, 8, 8), **shp)]
+    s = torch.empty(nb, **shp)
+    e = torch.empty(nb, dtype=torch.int32, device="cuda")
+    B.hydro_fused(Ud, v, None, nb, floor, gamma, *F, s, e)
+    Fh = [f.cpu().numpy() for f in F]
+    for i in range(nb):
+        fx, fy, fz, sm, code, cell = O.flux(O.reconstruct(U[i], floor), gamma)
+        assert K.decode_flux_error(int(e[i].cpu().numpy().view(np.uint32))) == (code, cell), i
+        if code == 0:  # on an error the reference discards the outputs
+            assert same(Fh[0][i], fx) and same(Fh[1][i], fy) and same(Fh[2][i], fz), i
+            assert same(s[i].item(), sm), i
 
 
 def _error_blocks(nb, seed, gamma):
