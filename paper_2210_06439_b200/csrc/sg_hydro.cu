@@ -1174,12 +1174,26 @@ hydro_update_kernel(FieldView uv, const int32_t* __restrict__ leaves, const doub
     const double* fx = FX + b * 5 * 576 + (z * 8 + y) * 9 + x;
     const double* fy = FY + b * 5 * 576 + (z * 9 + y) * 8 + x;
     const double* fz = FZ + b * 5 * 576 + (z * 8 + y) * 8 + x;
-    double rho = 0.0, en = 0.0;
+    // every load issued before the first store (u may alias nothing here, but
+    // the compiler cannot know: loads after a store would wait for it -- five
+    // serialised memory round trips per thread, 64% of HBM)
+    double f[NVAR][6], uo[NVAR];
 #pragma unroll
     for (int v = 0; v < NVAR; ++v) {
         const int64_t o = v * 576;
-        const double net = add(add(sub(fx[o + 1], fx[o]), sub(fy[o + 8], fy[o])), sub(fz[o + 64], fz[o]));
-        const double nu = sub(u[v * uv.comp_stride], mul(dtdx, net));
+        f[v][0] = __ldg(fx + o + 1);
+        f[v][1] = __ldg(fx + o);
+        f[v][2] = __ldg(fy + o + 8);
+        f[v][3] = __ldg(fy + o);
+        f[v][4] = __ldg(fz + o + 64);
+        f[v][5] = __ldg(fz + o);
+        uo[v] = u[v * uv.comp_stride];
+    }
+    double rho = 0.0, en = 0.0;
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) {
+        const double net = add(add(sub(f[v][0], f[v][1]), sub(f[v][2], f[v][3])), sub(f[v][4], f[v][5]));
+        const double nu = sub(uo[v], mul(dtdx, net));
         u[v * uv.comp_stride] = nu;
         if (v == 0) rho = nu;
         if (v == 4) en = nu;
@@ -1224,8 +1238,16 @@ max_wavespeed_kernel(FieldView uv, const int32_t* __restrict__ leaves, double ga
     if (fabs(vy) > av) av = fabs(vy);
     if (fabs(vz) > av) av = fabs(vz);
     const double s = add(av, c);
-    // reference: `if s > smax: smax = s` from 0.0 -> max over non-NaN s >= 0
-    if (s > 0.0) atomicMax(&s_max, (unsigned long long)__double_as_longlong(s));
+    // reference: `if s > smax: smax = s` from 0.0 -> max over non-NaN s >= 0;
+    // positive doubles order like their bit patterns: warp max, then one
+    // shared atomic per warp (not 512 on one address)
+    unsigned long long key = s > 0.0 ? (unsigned long long)__double_as_longlong(s) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, key, o);
+        key = k2 > key ? k2 : key;
+    }
+    if ((t & 31) == 0 && key) atomicMax(&s_max, key);
     __syncthreads();
     if (t == 0) out[b] = __longlong_as_double((long long)s_max);
 }

@@ -51,4 +51,7 @@ res = {
                                            u.flux_err)),
     "max_wavespeed": t(lambda: B.max_wavespeed(u.U, u.uv, u.leaves, u.nleaves, 1.4, 1e-12, u.ws)),
 }
+st = torch.empty(u.nleaves, dtype=torch.int32, device=u.U.device)
+res["hydro_update"] = t(lambda: B.hydro_update(u.U, u.uv, u.leaves, u.nleaves, u.FX, u.FY, u.FZ, None, None, 1e-9,
+                                               u.dx, 0.4, st))
 print(json.dumps({k: round(v, 4) for k, v in res.items()}))
