@@ -108,6 +108,17 @@ int finish(const char* fn, cudaStream_t st) {
 
 using namespace sg;
 
+// the 8^3 interiors of the 5 stacked (12, 12, 12) blocks, row by row:
+// what max_wavespeed reads and hydro_update reads and writes (20 KB of 69 KB)
+static void copy_interiors(double* dst, const double* src) {
+    for (int v = 0; v < 5; ++v)
+        for (int z = 2; z < 10; ++z)
+            for (int y = 2; y < 10; ++y) {
+                const int64_t o = ((int64_t)(v * 12 + z) * 12 + y) * 12 + 2;
+                std::memcpy(dst + o, src + o, 8 * sizeof(double));
+            }
+}
+
 extern "C" {
 
 int sg_dropin_max_wavespeed(const double* U, double gamma, double pfloor, double* smax, void* stream) {
@@ -117,9 +128,9 @@ int sg_dropin_max_wavespeed(const double* U, double gamma, double pfloor, double
     const size_t ub = sizeof(double) * U_DOUBLES;
     Stage* s;
     SG_TRY(stage_for(up(ub) + 64, 0, &s));
-    std::memcpy(s->h, U, ub);
-    // zero-copy: the kernel reads each cell once from the mapped buffer and
-    // writes the one result there
+    copy_interiors(reinterpret_cast<double*>(s->h), U);
+    // zero-copy: the kernel reads each interior cell once from the mapped
+    // buffer and writes the one result there
     double* hS = reinterpret_cast<double*>(s->h + up(ub));
     SG_TRY(sg_max_wavespeed(reinterpret_cast<double*>(s->hd), 8, 8, 8, 2, 0, nullptr, 1, gamma, pfloor,
                             reinterpret_cast<double*>(s->hd + up(ub)), stream));
@@ -224,13 +235,13 @@ int sg_dropin_hydro_update(double* U, const double* FX, const double* FY, const 
     const size_t ub = sizeof(double) * U_DOUBLES;
     Stage* s;
     SG_TRY(stage_for(up(ub) + 16, 0, &s));
-    std::memcpy(s->h, U, ub);
+    copy_interiors(reinterpret_cast<double*>(s->h), U);
     // zero-copy: every interior value is read and rewritten once in place
     SG_TRY(sg_hydro_update(reinterpret_cast<double*>(s->hd), 8, 8, 8, 2, 0, nullptr, 1, FX, FY, FZ, nullptr,
                            nullptr, dt, dx, cfl, reinterpret_cast<uint32_t*>(s->hd + up(ub)), nullptr, nullptr, 0,
                            nullptr, stream));
     SG_TRY(finish("sg_dropin_hydro_update", st));
-    std::memcpy(U, s->h, ub);
+    copy_interiors(U, reinterpret_cast<const double*>(s->h));
     std::memcpy(status, s->h + up(ub), 4);
     return SG_OK;
 }

@@ -194,6 +194,7 @@ def run_scenario(cfg: ScenarioConfig, backend: str = "scalar", threads: int = 1,
                       legacy_flux=hydro_kernel == "legacy")
     st.load({name: global_field(tree, name) for name in HYDRO_FIELDS})
     st.timers = {}
+    st.overlap_p2p = False  # every kernel timed on its own, as the reference's profile
     launches0 = _lib.launch_count()
     torch.cuda.synchronize()
     t0 = time.perf_counter_ns()

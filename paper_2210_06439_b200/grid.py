@@ -20,6 +20,7 @@ and dt computed on device.  Results are bit-identical to the reference loop.
 from __future__ import annotations
 
 import functools
+import os
 
 import numpy as np
 import torch
@@ -117,6 +118,12 @@ class UnigridState:
         self.step_index = 0      # timesteps started since load()
         self._iter_step = []     # hydro iteration -> timestep index
         self.timers = None  # optional {kernel: [(start, end) events]} for per-kernel timing
+        # P2P beside M2L on a side stream (see gravity_kernels); its launches
+        # are not timed then (an event pair would include the wait for the
+        # M2L tail)
+        self.overlap_p2p = os.environ.get("SG_P2P_OVERLAP", "1") != "0"  # "0": serial (A/B tooling)
+        self._side = None
+        self._grav_p2p = None
 
     # -- host <-> device ---------------------------------------------------
 
@@ -236,17 +243,51 @@ class UnigridState:
 
     @_on_device
     def gravity_kernels(self) -> None:
+        """cluster aggregation, P2P and M2L of one gravity iteration.
+
+        In the reference the monopole result is overwritten by the multipole
+        one (driver.py:123-139): P2P's output is dead, its inputs are M2L's.
+        So P2P runs on a side stream into its own buffer (p2p_result()),
+        launched right after M2L: the persistent M2L kernel holds every SM
+        (one CTA filling the register file) and P2P's CTAs take the SMs the
+        M2L tail leaves idle (4096 subgrids = 27 full rounds + 100 on 148
+        SMs).  The main stream waits for P2P before anything that rewrites
+        the masses.  Same work, same bits in phi/g."""
         ev = self._t("cluster_aggregate")
         B.cluster_aggregate(self.mass, self.dx, self.clusters)
         self._done(ev)
-        ev = self._t("p2p")
-        B.p2p(self.mass, self.mv, self.leaves, self.nleaves, self.dx, self.rad2, self.eps2, self.halo,
-              self.grav, self.gv, precision=self.precision)
-        self._done(ev)
+        if not self.overlap_p2p:
+            ev = self._t("p2p")
+            B.p2p(self.mass, self.mv, self.leaves, self.nleaves, self.dx, self.rad2, self.eps2, self.halo,
+                  self.grav, self.gv, precision=self.precision)
+            self._done(ev)
+            self._m2l()
+            return
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+            self._ev_in = torch.cuda.Event()
+            self._ev_p2p = torch.cuda.Event()
+            self._grav_p2p = torch.empty_like(self.grav)
+        main = torch.cuda.current_stream(self.device)
+        self._ev_in.record(main)
+        self._m2l()
+        self._side.wait_event(self._ev_in)
+        with torch.cuda.stream(self._side):
+            B.p2p(self.mass, self.mv, self.leaves, self.nleaves, self.dx, self.rad2, self.eps2, self.halo,
+                  self._grav_p2p, self.gv, precision=self.precision)
+            self._ev_p2p.record(self._side)
+        main.wait_event(self._ev_p2p)
+
+    def _m2l(self) -> None:
         ev = self._t("m2l")
         B.m2l(self.mass, self.mv, self.clusters, 0, self.leaves, self.nleaves, self.dx, self.rad2, self.eps2,
               self.g.expansion_order, self.grav, self.gv, precision=self.precision)
         self._done(ev)
+
+    def p2p_result(self) -> torch.Tensor:
+        """(phi, gx, gy, gz) of the last gravity iteration's P2P (monopole)
+        pass, which phi/g (the multipole result) overwrite in the reference."""
+        return self._grav_p2p if self._grav_p2p is not None and self.overlap_p2p else self.grav
 
     @_on_device
     def wavespeed_dt(self) -> None:

@@ -183,6 +183,24 @@ class TestStatusWords:
         assert K.decode_flux_error((key << 12) | (2 << 10) | 987) == (2, 987)
 
 
+def test_stacked_hydro_block_is_shared_until_a_field_is_replaced():
+    """SubGrid.allocate keeps the hydro fields as views of one (5, 12, 12, 12)
+    block, which the drop-in calls pass to the library without a copy; a
+    replaced field array falls back to a stacked copy with the same values."""
+    leaf = build_unigrid(1).leaves[3]
+    rng = np.random.default_rng(0)
+    for name in K.HYDRO_FIELDS:
+        leaf.fields[name][...] = rng.uniform(size=(EXT, EXT, EXT))
+    want = np.stack([leaf.fields[n] for n in K.HYDRO_FIELDS])
+    blk = K._stack_hydro(leaf)
+    assert blk is leaf.hydro_block and np.array_equal(blk, want)
+    leaf.fields["sy"] = leaf.fields["sy"].copy()
+    leaf.fields["sy"][0, 0, 0] = -1.0
+    want[2, 0, 0, 0] = -1.0
+    U = K._stack_hydro(leaf)
+    assert U is not leaf.hydro_block and np.array_equal(U, want)
+
+
 def test_source_cube_is_periodic_window_of_global_field():
     """octree.source_cube (reference octree.py:186-214) == the periodic
     (8+2h)^3 window of the global field around the leaf, every halo 0..8."""
