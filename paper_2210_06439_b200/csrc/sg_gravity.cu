@@ -156,8 +156,7 @@ __device__ __forceinline__ void k8_all(const double* col, const P2PStencil& st, 
 
 // all 8 targets of the thread's column (x, y, 0..7) with the K8 shortcuts,
 // written to o (z stride sz, component stride cs); NT targets per pass over
-// the 92 unrolled entries (ILP vs registers: 4 on the 255-register double-
-// buffered kernel, 103.7 vs 105.3 us at L=4; 2 under the 128-register cap)
+// the 92 unrolled entries (2 fit the 128-register cap of 8 CTAs per SM)
 template <int NT>
 __device__ __forceinline__ void k8_column(const double* col, const P2PStencil& st, double* o, int64_t sz,
                                           int64_t cs) {
@@ -380,93 +379,6 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
             ok[3 * ov.comp_stride] = az[k];
         }
         }
-    }
-}
-
-// Double-buffered TMA variant: the next subgrid's cube is requested (one
-// tile copy) before the current one is computed, so no CTA waits on its
-// staging; 2 x 27.6 KB of shared memory -> 4 CTAs per SM, and 4096 subgrids
-// then tile 592 CTAs as 6.9 rounds (a lighter last round than 3.5 x 1184).
-template <bool FAST>
-__global__ void __launch_bounds__(P2P_PARAM_THREADS, 4)
-p2p_tma2_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, int halo, FieldView ov,
-                const __grid_constant__ P2PStencil st, const __grid_constant__ CUtensorMap tm) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int S = NIN + 2 * halo;
-    const int pitch = p2p_pitch(S);
-    const int plane = pitch * S;
-    double* const cube0 = reinterpret_cast<double*>(smem_raw);
-    uint64_t* const bar = reinterpret_cast<uint64_t*>(cube0 + 2 * S * plane);  // [2]
-    const int tid = threadIdx.x;
-    const int x = tid & 7, y = tid >> 3;
-    const int col0 = halo * plane + (y + halo) * pitch + (x + halo);  // target (x, y, 0) in a buffer
-    const unsigned bytes = (unsigned)(sizeof(double) * S * plane);
-    auto request = [&](int64_t b, int buf) {  // one elected thread
-        int64_t cx = mv.pad - halo, cy = mv.pad - halo, cz = mv.pad - halo;
-        if (leaves) {
-            cx += 8 * (int64_t)leaves[3 * b];
-            cy += 8 * (int64_t)leaves[3 * b + 1];
-            cz += 8 * (int64_t)leaves[3 * b + 2];
-        } else {
-            cz += b * (mv.leaf_stride / mv.sz);
-        }
-        tma_expect_tx(bar + buf, bytes);
-        tma_load_3d(cube0 + buf * S * plane, &tm, (int)cx, (int)cy, (int)cz, bar + buf);
-    };
-    if (tid == 0) {
-        tma_mbar_init(bar, 1);
-        tma_mbar_init(bar + 1, 1);
-        if (blockIdx.x < B) request(blockIdx.x, 0);
-    }
-    __syncthreads();
-    unsigned phases = 0;  // bit i: phase of buffer i
-    int it = 0;
-    for (int64_t b = blockIdx.x; b < B; b += gridDim.x, ++it) {
-        const int cur = it & 1;
-        // the other buffer was last read in the previous iteration, closed by its barrier
-        if (tid == 0 && b + gridDim.x < B) request(b + gridDim.x, cur ^ 1);
-        tma_wait(bar + cur, (phases >> cur) & 1u);
-        phases ^= 1u << cur;
-        const double* const col = cube0 + cur * S * plane + col0;
-        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + y * ov.sy + x;
-        // K8 shortcut (exact mode) unless some mass of this cube is out of its range
-        if (!FAST && st.k8 && !__syncthreads_or(k8_cube_bad(cube0 + cur * S * plane, st.elo, st.ehi, tid, P2P_PARAM_THREADS))) {
-            k8_column<4>(col, st, o, ov.sz, ov.comp_stride);
-        } else {
-        double ap[P2P_TPT], ax[P2P_TPT], ay[P2P_TPT], az[P2P_TPT];
-#pragma unroll
-        for (int k = 0; k < P2P_TPT; ++k) ap[k] = ax[k] = ay[k] = az[k] = 0.0;
-#pragma unroll 4
-        for (int e = 0; e < st.count; ++e) {
-            const int d = st.delta[e];
-            const double inv = st.inv[e], inv3 = st.inv3[e], rx = st.rx[e], ry = st.ry[e], rz = st.rz[e];
-#pragma unroll
-            for (int k = 0; k < P2P_TPT; ++k) {
-                const double m = col[k * plane + d];
-                const double c = mul(m, inv3);
-                if (FAST) {
-                    ap[k] = __fma_rn(-m, inv, ap[k]);
-                    ax[k] = __fma_rn(-c, rx, ax[k]);
-                    ay[k] = __fma_rn(-c, ry, ay[k]);
-                    az[k] = __fma_rn(-c, rz, az[k]);
-                } else {
-                    ap[k] = add(ap[k], -mul(m, inv));
-                    ax[k] = add(ax[k], -mul(c, rx));
-                    ay[k] = add(ay[k], -mul(c, ry));
-                    az[k] = add(az[k], -mul(c, rz));
-                }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < P2P_TPT; ++k) {
-            double* ok = o + k * ov.sz;
-            ok[0] = ap[k];
-            ok[ov.comp_stride] = ax[k];
-            ok[2 * ov.comp_stride] = ay[k];
-            ok[3 * ov.comp_stride] = az[k];
-        }
-        }
-        __syncthreads();  // this buffer's reads are done before it is refilled
     }
 }
 
@@ -2139,22 +2051,11 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
             kern<<<(unsigned)pgrid, P2P_PARAM_THREADS, smem_t, (cudaStream_t)stream>>>(mv, leaves, nleaves, halo,
                                                                                        ov, st, tm);
         };
-        // double buffering pays for large batches (4096 subgrids: 0.149 -> 0.144 ms); with fewer
-        // subgrids than 2 rounds of 8 CTAs per SM the single-buffer kernel's occupancy wins
-        static const bool single = getenv("SG_P2P_TMA_SINGLE") != nullptr;  // A/B tooling
-        if (tma && !single && nleaves >= 2 * cap) {
-            const int64_t cap2 = 4 * (int64_t)sm_count();
-            const int64_t grid2 = nleaves < cap2 ? nleaves : cap2;
-            const size_t smem2 = 2 * smem + 16;
-            auto go2 = [&](auto kern) {
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-                sg_count_launch(1);
-                kern<<<(unsigned)grid2, P2P_PARAM_THREADS, smem2, (cudaStream_t)stream>>>(mv, leaves, nleaves, halo,
-                                                                                         ov, st, tm);
-            };
-            if (precision == SG_PREC_FMA) go2(p2p_tma2_kernel<true>);
-            else go2(p2p_tma2_kernel<false>);
-        } else if (precision == SG_PREC_FMA) {
+        // (a double-buffered variant -- the next subgrid's tile requested before
+        // the current one is computed, 4 CTAs per SM -- paid with the 9-op loop,
+        // 0.149 -> 0.144 ms at 4096 subgrids; with the K8 shortcut these 8 CTAs
+        // per SM win, 93.2 vs 101.7 us exact, 86.4 vs 87.3 FMA: removed in r2l)
+        if (precision == SG_PREC_FMA) {
             tma ? go(p2p_param_kernel<true, true>) : go(p2p_param_kernel<true, false>);
         } else {
             tma ? go(p2p_param_kernel<false, true>) : go(p2p_param_kernel<false, false>);

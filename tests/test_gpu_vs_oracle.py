@@ -50,8 +50,8 @@ def test_m2l_p2p_random_cubes(dx, theta, eps, order):
 
 @pytest.mark.parametrize("nb,dx", [(64, 1.0 / 64), (2400, 1.0 / 128), (64, 0.1)])
 def test_p2p_batched_edge_masses_vs_oracle(nb, dx):
-    """Batched P2P (the persistent stencil kernels: 64 subgrids take the
-    single-buffer TMA kernel, 2400 the double-buffered one) bitwise against
+    """Batched P2P (the persistent TMA-staged stencil kernel: 64 subgrids in
+    one partial round, 2400 in several rounds per CTA) bitwise against
     the oracle per subgrid, with cubes aimed at the exact K8 shortcut's
     guards: zeros (+/-), NaN, inf, subnormal and huge masses, masses at the
     edges of the shortcut's exponent range; dx = 0.1 (not a power of two)
@@ -139,10 +139,10 @@ def test_hydro_random_blocks(gamma, floor, seed):
 
 
 def _edge_blocks(gamma):
-    """Hydro blocks aimed at the fused kernel's exact shortcuts (direction
-    folding, shared-reciprocal kinetic energy): -0.0 centre values under
-    zero slopes (the zero-sum sign reaches u + 0.5*sum), +0.0 momenta,
-    infinite slopes, and magnitudes outside 2^+-500 / subnormal."""
+    """Hydro blocks with the values exact arithmetic shortcuts get wrong
+    (DESIGN.md 9.2 measured two for the fused kernel): -0.0 centre values
+    under zero slopes (the zero-sum sign reaches u + 0.5*sum), +0.0
+    momenta, infinite slopes, and magnitudes outside 2^+-500 / subnormal."""
     rng = np.random.default_rng(77)
     out = []
     for kind in range(8):
