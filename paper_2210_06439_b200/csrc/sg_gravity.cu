@@ -154,14 +154,14 @@ __device__ __forceinline__ void k8_all(const double* col, const P2PStencil& st, 
 }
 
 
-// all 8 targets of the thread's column (x, y, 0..7) with the K8 shortcuts,
+// the thread's TPT targets of column (x, y) with the K8 shortcuts,
 // written to o (z stride sz, component stride cs); NT targets per pass over
 // the 92 unrolled entries (2 fit the 128-register cap of 8 CTAs per SM)
-template <int NT>
+template <int NT, int TPT>
 __device__ __forceinline__ void k8_column(const double* col, const P2PStencil& st, double* o, int64_t sz,
                                           int64_t cs) {
 #pragma unroll 1
-    for (int k0 = 0; k0 < 8; k0 += NT) {
+    for (int k0 = 0; k0 < TPT; k0 += NT) {
         double p[NT], x[NT], y[NT], z[NT];
 #pragma unroll
         for (int k = 0; k < NT; ++k) p[k] = x[k] = y[k] = z[k] = 0.0;
@@ -256,9 +256,7 @@ __device__ int p2p_build_chunk(P2PEntry* ent, int* warp_cnt, int c0, int halo, d
 // next leaf overlaps the others' compute.  Measured at L=4 (exact / FMA):
 // 2 targets per thread 0.166 / 0.132 ms, 4 per thread (double-buffered)
 // 0.164 / 0.125 ms, this 0.163 / 0.120 ms.
-constexpr int P2P_TPT = 8;
-constexpr int P2P_PARAM_THREADS = 512 / P2P_TPT;
-constexpr int P2P_PARAM_CTAS_PER_SM = 8;
+constexpr int P2P_PARAM_CTAS_PER_SM = 8;  // for TPT = 8 (64 threads); TPT = 4: 4 CTAs of 128
 // TMA helpers (cp.async.bulk.tensor + mbarrier completion)
 __device__ __forceinline__ void tma_mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
@@ -295,8 +293,11 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 // box {pitch, S, S} (x rows padded to the conflict-free pitch; the extra
 // columns are neighbours or zero-filled out of bounds) instead of S^3 8-byte
 // cp.async requests; completion on an mbarrier (phase = leaf parity).
-template <bool FAST, bool TMA>
-__global__ void __launch_bounds__(P2P_PARAM_THREADS, P2P_PARAM_CTAS_PER_SM)
+// TPT targets per thread: 8 (64 threads, one per (x, y) column) when the
+// batch fills 8 CTAs per SM; 4 (128 threads, two per column) for batches of
+// one partial round, which would otherwise leave most warp slots empty
+template <bool FAST, bool TMA, int TPT>
+__global__ void __launch_bounds__(512 / TPT, TPT == 8 ? 8 : 4)
 p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, int halo, FieldView ov,
                  const __grid_constant__ P2PStencil st, const __grid_constant__ CUtensorMap tm) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -305,9 +306,10 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
     const int plane = pitch * S;
     double* const cube = reinterpret_cast<double*>(smem_raw);
     uint64_t* bar = reinterpret_cast<uint64_t*>(cube + S * plane);
+    constexpr int NTH = 512 / TPT;
     const int tid = threadIdx.x;
-    const int x = tid & 7, y = tid >> 3;
-    const double* const col = cube + halo * plane + (y + halo) * pitch + (x + halo);  // target (x, y, 0)
+    const int x = tid & 7, y = (tid >> 3) & 7, z0 = (tid >> 6) * TPT;
+    const double* const col = cube + (z0 + halo) * plane + (y + halo) * pitch + (x + halo);  // target (x, y, z0)
     if (TMA && tid == 0) tma_mbar_init(bar, 1);
     unsigned phase = 0;
     for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
@@ -331,7 +333,7 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
             phase ^= 1u;
         } else {
             const double* src = leaf_origin(mv, leaves, b, halo);
-            for (int i = tid; i < S * S * S; i += P2P_PARAM_THREADS) {
+            for (int i = tid; i < S * S * S; i += NTH) {
                 const int cx = i % S, cy = (i / S) % S, cz = i / (S * S);
                 const unsigned dst = (unsigned)__cvta_generic_to_shared(cube + cz * plane + cy * pitch + cx);
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
@@ -341,20 +343,20 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
             asm volatile("cp.async.commit_group;\n" "cp.async.wait_group 0;\n" ::: "memory");
             __syncthreads();
         }
-        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + y * ov.sy + x;
+        double* o = const_cast<double*>(leaf_origin(ov, leaves, b, 0)) + z0 * ov.sz + y * ov.sy + x;
         // K8 shortcut (exact mode) unless some mass of this cube is out of its range
-        if (!FAST && st.k8 && !__syncthreads_or(k8_cube_bad(cube, st.elo, st.ehi, tid, P2P_PARAM_THREADS))) {
-            k8_column<2>(col, st, o, ov.sz, ov.comp_stride);
+        if (!FAST && st.k8 && !__syncthreads_or(k8_cube_bad(cube, st.elo, st.ehi, tid, NTH))) {
+            k8_column<2, TPT>(col, st, o, ov.sz, ov.comp_stride);
         } else {
-        double ap[P2P_TPT], ax[P2P_TPT], ay[P2P_TPT], az[P2P_TPT];
+        double ap[TPT], ax[TPT], ay[TPT], az[TPT];
 #pragma unroll
-        for (int k = 0; k < P2P_TPT; ++k) ap[k] = ax[k] = ay[k] = az[k] = 0.0;
+        for (int k = 0; k < TPT; ++k) ap[k] = ax[k] = ay[k] = az[k] = 0.0;
 #pragma unroll 4
         for (int e = 0; e < st.count; ++e) {
             const int d = st.delta[e];
             const double inv = st.inv[e], inv3 = st.inv3[e], rx = st.rx[e], ry = st.ry[e], rz = st.rz[e];
 #pragma unroll
-            for (int k = 0; k < P2P_TPT; ++k) {
+            for (int k = 0; k < TPT; ++k) {
                 const double m = col[k * plane + d];
                 const double c = mul(m, inv3);
                 if (FAST) {  // FMA-contracted: 5 DP instructions per pair instead of 9
@@ -371,7 +373,7 @@ p2p_param_kernel(FieldView mv, const int32_t* __restrict__ leaves, int64_t B, in
             }
         }
 #pragma unroll
-        for (int k = 0; k < P2P_TPT; ++k) {
+        for (int k = 0; k < TPT; ++k) {
             double* ok = o + k * ov.sz;
             ok[0] = ap[k];
             ok[ov.comp_stride] = ax[k];
@@ -2045,20 +2047,26 @@ int sg_p2p(const double* mass, int64_t nx, int64_t ny, int64_t nz, int32_t pad, 
                                         (nz + 2 * pad) * (leaves ? 1 : nleaves), leaf_stride, nx + 2 * pad, ny + 2 * pad,
                                         nz + 2 * pad, S, p2p_pitch(S));
         const size_t smem_t = smem + 16;  // + the mbarrier
-        auto go = [&](auto kern) {
+        // a batch short of one full round of 8 CTAs per SM: 4 targets per thread
+        // (twice the warps per subgrid)
+        static const bool no_t4 = getenv("SG_P2P_NO_T4") != nullptr;  // A/B tooling
+        const bool t4 = nleaves < cap && !no_t4;
+        auto go = [&](auto kern, int threads) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
             sg_count_launch(1);
-            kern<<<(unsigned)pgrid, P2P_PARAM_THREADS, smem_t, (cudaStream_t)stream>>>(mv, leaves, nleaves, halo,
-                                                                                       ov, st, tm);
+            kern<<<(unsigned)pgrid, threads, smem_t, (cudaStream_t)stream>>>(mv, leaves, nleaves, halo, ov, st, tm);
         };
+        auto go2 = [&](auto k8t, auto k4t) { t4 ? go(k4t, 128) : go(k8t, 64); };
         // (a double-buffered variant -- the next subgrid's tile requested before
         // the current one is computed, 4 CTAs per SM -- paid with the 9-op loop,
         // 0.149 -> 0.144 ms at 4096 subgrids; with the K8 shortcut these 8 CTAs
         // per SM win, 93.2 vs 101.7 us exact, 86.4 vs 87.3 FMA: removed in r2l)
         if (precision == SG_PREC_FMA) {
-            tma ? go(p2p_param_kernel<true, true>) : go(p2p_param_kernel<true, false>);
+            tma ? go2(p2p_param_kernel<true, true, 8>, p2p_param_kernel<true, true, 4>)
+                : go2(p2p_param_kernel<true, false, 8>, p2p_param_kernel<true, false, 4>);
         } else {
-            tma ? go(p2p_param_kernel<false, true>) : go(p2p_param_kernel<false, false>);
+            tma ? go2(p2p_param_kernel<false, true, 8>, p2p_param_kernel<false, true, 4>)
+                : go2(p2p_param_kernel<false, false, 8>, p2p_param_kernel<false, false, 4>);
         }
         return sg_check_launch("sg_p2p");
     }
