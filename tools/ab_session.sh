@@ -1,8 +1,5 @@
-# ad-hoc A/B session (edited per experiment): P2P double-buffered (4 CTAs/SM,
-# 4 targets per pass) vs single-buffer TMA kernel (8 CTAs/SM, 2 per pass),
-# then the bounds-checked build over the GPU suite
-for i in 1 2; do
-python tools/p2p_time.py 4 40
-SG_P2P_TMA_SINGLE=1 python tools/p2p_time.py 4 40
-done
-bash tools/debug_bounds.sh
+# ad-hoc A/B session (edited per experiment): GPU tests on the default build,
+# then the fused hydro of every libsg_*.so variant vs the default
+python -m pytest tests -m gpu -q > gpurun_out/tests_ab.log 2>&1; tail -2 gpurun_out/tests_ab.log
+bash tools/ab_hydro_libs.sh 4
+bash tools/ab_hydro_libs.sh 3
