@@ -64,45 +64,48 @@ namespace sg {
 // fill has no read/write overlap.  A non-wrapped axis keeps its coordinate:
 // in z-slab mode (mask 3) region A is skipped -- those planes arrive whole
 // from the neighbour ranks after this fill.
-__global__ void fill_periodic_kernel(double* __restrict__ f, int64_t ncomp, int64_t nx, int64_t ny,
-                                     int64_t nz, int pad, int wrap_mask) {
-    const int64_t X = nx + 2 * pad, Y = ny + 2 * pad, Z = nz + 2 * pad;
-    const int64_t vol = X * Y * Z;
+// I: index type -- 32-bit whenever every flat index fits (64-bit divisions
+// are emulated in tens of instructions: 16 -> 4 us per fill at level 4)
+template <typename I>
+__global__ void fill_periodic_kernel(double* __restrict__ f, I ncomp, I nx, I ny, I nz, int pad, int wrap_mask) {
+    const I X = nx + 2 * pad, Y = ny + 2 * pad, Z = nz + 2 * pad;
+    const int64_t vol = (int64_t)X * Y * Z;
     const bool wz = wrap_mask & 4;
-    const int64_t nA = wz ? 2 * pad * Y * X : 0, nB = nz * 2 * pad * X, nC = nz * ny * 2 * pad;
-    const int64_t per = nA + nB + nC;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= per * ncomp) return;
-    const int64_t c = i / per;
-    int64_t r = i % per, x, y, z;
+    const I nA = wz ? 2 * pad * Y * X : 0, nB = nz * 2 * pad * X, nC = nz * ny * 2 * pad;
+    const I per = nA + nB + nC;
+    const int64_t i64 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i64 >= (int64_t)per * ncomp) return;
+    const I i = (I)i64;
+    const I c = i / per;
+    I r = i % per, x, y, z;
     if (r < nA) {
         x = r % X;
         y = (r / X) % Y;
-        const int64_t zp = r / (X * Y);
+        const I zp = r / (X * Y);
         z = zp < pad ? zp : nz + zp;
     } else if ((r -= nA) < nB) {
         x = r % X;
-        const int64_t yp = (r / X) % (2 * pad);
+        const I yp = (r / X) % (2 * pad);
         y = yp < pad ? yp : ny + yp;
         z = pad + r / (X * 2 * pad);
     } else {
         r -= nB;
-        const int64_t xp = r % (2 * pad);
+        const I xp = r % (2 * pad);
         x = xp < pad ? xp : nx + xp;
         y = pad + (r / (2 * pad)) % ny;
         z = pad + r / (2 * pad * ny);
     }
-    auto wrapc = [pad](int64_t v, int64_t n) {
-        int64_t w = (v - pad) % n;
+    auto wrapc = [pad](I v, I n) {
+        I w = (v - pad) % n;
         if (w < 0) w += n;
         return w + pad;
     };
     const bool ix = x >= pad && x < pad + nx, iy = y >= pad && y < pad + ny, iz = z >= pad && z < pad + nz;
-    const int64_t sx = (!ix && (wrap_mask & 1)) ? wrapc(x, nx) : x;
-    const int64_t sy = (!iy && (wrap_mask & 2)) ? wrapc(y, ny) : y;
-    const int64_t sz = (!iz && wz) ? wrapc(z, nz) : z;
+    const I sx = (!ix && (wrap_mask & 1)) ? wrapc(x, nx) : x;
+    const I sy = (!iy && (wrap_mask & 2)) ? wrapc(y, ny) : y;
+    const I sz = (!iz && wz) ? wrapc(z, nz) : z;
     if (sx == x && sy == y && sz == z) return;
-    f[c * vol + (z * Y + y) * X + x] = f[c * vol + (sz * Y + sy) * X + sx];
+    f[c * vol + ((int64_t)z * Y + y) * X + x] = f[c * vol + ((int64_t)sz * Y + sy) * X + sx];
 }
 
 // dst interior (pad pd) = src interior (pad ps, component 0) * scale
@@ -162,8 +165,13 @@ int sg_fill_periodic(double* field, int64_t ncomp, int64_t nx, int64_t ny, int64
     if (total <= 0 || pad == 0) return SG_OK;
     SG_TRY(sg_check_ptr("sg_fill_periodic", "field", field));
     sg_count_launch(1);
-    fill_periodic_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        field, ncomp, nx, ny, nz, pad, wrap_mask);
+    const int64_t Z = nz + 2 * pad;
+    if (total < INT32_MAX && X * Y * Z < INT32_MAX)
+        fill_periodic_kernel<int32_t><<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+            field, (int32_t)ncomp, (int32_t)nx, (int32_t)ny, (int32_t)nz, pad, wrap_mask);
+    else
+        fill_periodic_kernel<int64_t><<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+            field, ncomp, nx, ny, nz, pad, wrap_mask);
     return sg_check_launch("sg_fill_periodic");
 }
 
