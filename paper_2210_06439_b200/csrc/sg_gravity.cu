@@ -40,7 +40,17 @@ __global__ void cluster_aggregate_kernel(const double* __restrict__ mass, int64_
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t total = ncx * ncy * ncz;
     if (i >= total) return;
-    int64_t cx = i % ncx, cy = (i / ncx) % ncy, cz = i / (ncx * ncy);
+    int64_t cx, cy, cz;
+    if (total < INT32_MAX) {  // 32-bit divisions (64-bit ones are emulated)
+        const uint32_t u = (uint32_t)i, nx = (uint32_t)ncx, ny = (uint32_t)ncy;
+        cx = u % nx;
+        cy = (u / nx) % ny;
+        cz = u / (nx * ny);
+    } else {
+        cx = i % ncx;
+        cy = (i / ncx) % ncy;
+        cz = i / (ncx * ncy);
+    }
     double m_tot = 0.0, dxa = 0.0, dya = 0.0, dza = 0.0;
 #pragma unroll
     for (int o = 0; o < 8; ++o) {

@@ -113,7 +113,17 @@ __global__ void scale_copy_kernel(double* __restrict__ dst, int pd, const double
                                   int64_t nx, int64_t ny, int64_t nz, double scale) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nx * ny * nz) return;
-    const int64_t x = i % nx, y = (i / nx) % ny, z = i / (nx * ny);
+    int64_t x, y, z;
+    if (nx * ny * nz < INT32_MAX) {  // 32-bit divisions (64-bit ones are emulated)
+        const uint32_t u = (uint32_t)i, ux = (uint32_t)nx, uy = (uint32_t)ny;
+        x = u % ux;
+        y = (u / ux) % uy;
+        z = u / (ux * uy);
+    } else {
+        x = i % nx;
+        y = (i / nx) % ny;
+        z = i / (nx * ny);
+    }
     const int64_t Xd = nx + 2 * pd, Yd = ny + 2 * pd, Xs = nx + 2 * ps, Ys = ny + 2 * ps;
     dst[((z + pd) * Yd + (y + pd)) * Xd + (x + pd)] = mul(src[((z + ps) * Ys + (y + ps)) * Xs + (x + ps)], scale);
 }
