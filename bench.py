@@ -574,7 +574,7 @@ def run_ours(args) -> None:
     # P2P runs beside M2L on a side stream in the timed steps (grid.py
     # gravity_kernels), where an event pair would time its wait for the M2L
     # tail: its standalone launch time comes from a short serial pass
-    timers = u.timers
+    timers, overlap = u.timers, u.overlap_p2p
     u.load(state)
     barrier()
     u.timers, u.overlap_p2p = {}, False
@@ -583,7 +583,7 @@ def run_ours(args) -> None:
     barrier()
     u.check_errors()
     timers["p2p"] = u.timers["p2p"]
-    u.timers, u.overlap_p2p = timers, True
+    u.timers, u.overlap_p2p = timers, overlap
     per_kernel = {}
     for name, evs in u.timers.items():
         ts = [a.elapsed_time(b) * 1e-3 for a, b in evs]

@@ -124,6 +124,7 @@ class UnigridState:
         self.overlap_p2p = os.environ.get("SG_P2P_OVERLAP", "1") != "0"  # "0": serial (A/B tooling)
         self._side = None
         self._grav_p2p = None
+        self._p2p_side = False   # the last gravity iteration ran P2P on the side stream
 
     # -- host <-> device ---------------------------------------------------
 
@@ -256,6 +257,7 @@ class UnigridState:
         ev = self._t("cluster_aggregate")
         B.cluster_aggregate(self.mass, self.dx, self.clusters)
         self._done(ev)
+        self._p2p_side = self.overlap_p2p
         if not self.overlap_p2p:
             ev = self._t("p2p")
             B.p2p(self.mass, self.mv, self.leaves, self.nleaves, self.dx, self.rad2, self.eps2, self.halo,
@@ -284,10 +286,12 @@ class UnigridState:
               self.g.expansion_order, self.grav, self.gv, precision=self.precision)
         self._done(ev)
 
-    def p2p_result(self) -> torch.Tensor:
+    def p2p_result(self) -> torch.Tensor | None:
         """(phi, gx, gy, gz) of the last gravity iteration's P2P (monopole)
-        pass, which phi/g (the multipole result) overwrite in the reference."""
-        return self._grav_p2p if self._grav_p2p is not None and self.overlap_p2p else self.grav
+        pass, which phi/g (the multipole result) overwrite in the reference;
+        None when that iteration ran serially (its P2P output went to phi/g
+        and was overwritten there, as in the reference)."""
+        return self._grav_p2p if self._p2p_side else None
 
     @_on_device
     def wavespeed_dt(self) -> None:
